@@ -1,0 +1,130 @@
+/*
+ * include/irk.h -- C ABI of the B200-native IRKGL16 integrator.
+ *
+ * The library integrates y' = f(t, y), y(t0) = y0 with constant step h
+ * ("t_n = t_0 + n h", "constant step-size
+ * mode") by the 8-stage, order-16 Gauss-Legendre collocation method (IRKGL16,
+ * P:L109-116) in the symplectic mu-form (Eqs. Yi2/yn2), solving the
+ * stage equations by the partitioned fixed-point iteration (Eqs. IRK_init2,
+ * IRK_FP2) or the first-order one (Eqs. IRK_init, IRK_FP,
+ * P:L218-232) with the stagnation stopping test (Eq. stopping, P:L239-244,
+ * reading R2 in DESIGN.md).  All arithmetic is IEEE binary64.
+ *
+ * Conventions
+ *  - Bulk-data pointers are CUDA DEVICE pointers owned by the caller, except in
+ *    irk_integrate_host (HOST pointers).  Nothing is retained after a call
+ *    returns except inside the ctx.
+ *  - y is structure-of-arrays, shape [dim][batch] (row l contiguous over
+ *    trajectories); component order (q_1..q_d, v_1..v_d), d = dim/2, v = M^-1 p
+ *    (P:L255-264).  N-body positions are body-major xyz (P:L394's (3,N) array).
+ *  - All device work is enqueued on `stream` (a cudaStream_t; NULL = legacy
+ *    default stream) and is asynchronous: buffers must stay alive until the
+ *    stream is synchronised.  Functions that must read device results
+ *    (irk_stats) synchronise the stream themselves.
+ *  - Errors: functions return an irk_status; argument errors are detected
+ *    synchronously and leave every buffer untouched.  irk_last_error() gives a
+ *    message.  A ctx is not thread-safe; distinct ctxs are independent.
+ */
+#ifndef IRK_H
+#define IRK_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct irk_ctx irk_ctx; /* opaque, owned by the library */
+
+/* Problems (right-hand sides g(q,t) of q' = v, v' = g(q,t), Eq. ivp2). */
+enum irk_problem {
+    IRK_KEPLER = 1,        /* planar Kepler, dim = 4; params {GM}                           */
+    IRK_NBODY = 2,         /* N-body Eq. Ham2, symmetric pairs, dim = 6N, N >= 2;
+                              params {G, eps, m_1..m_N}                                   */
+    IRK_FPU_BETA = 3,      /* FPU-beta chain, fixed ends, dim = 2N; params {beta}            */
+    IRK_HENON_HEILES = 4,  /* Listing 2, dim = 4; params {lambda, xi}          */
+    IRK_NBODY_DIRECT = 5   /* large-N direct sum, canonical blocked j-order, dim = 6N;
+                              params {G, eps > 0, m_1..m_N}; batch must be 1                */
+};
+
+enum irk_status {
+    IRK_OK = 0,
+    IRK_W_MAXITER = 1,    /* warning (irk_stats): some steps hit MAX_ITERS; results valid   */
+    IRK_E_ARG = -1,       /* invalid argument (returned synchronously)                      */
+    IRK_E_CUDA = -2,      /* a CUDA call failed                                             */
+    IRK_E_DIVERGED = -3,  /* (irk_stats) a trajectory became non-finite and was frozen      */
+    IRK_E_COMM = -4,      /* NCCL error                                                     */
+    IRK_E_STATE = -5      /* call out of order (e.g. integrate before set_params)           */
+};
+
+enum irk_option {
+    IRK_OPT_MODE = 1,         /* 0 = partitioned (default, Eq. IRK_FP2), 1 = first-order (Eq. IRK_FP) */
+    IRK_OPT_MAX_ITERS = 2,    /* sweeps cap per step, default 100 (flagged, step accepted)   */
+    IRK_OPT_ENERGY_EVERY = 3, /* E > 0: sample H(y_n) at local steps 0, E, 2E, ... (default 0) */
+    IRK_OPT_MAPPING = 4       /* 0 = auto; see DESIGN.md for the per-problem kernels          */
+};
+
+/* Create a context for `batch` independent trajectories of `problem` in
+ * dimension `dim`, step h (finite, != 0; negative allowed), nsteps >= 0 steps per
+ * irk_integrate call.  Builds the tableau in __float128 (Newton on P_8,
+ * Bjorck-Pereyra Vandermonde solves), checks B(16), C(8), the symplectic
+ * condition and the mu~ identity, and rounds it (R-1).  Returns NULL
+ * on error (message via irk_last_error(NULL)). */
+irk_ctx *irk_create(int problem, int dim, double h, int64_t nsteps, int64_t batch);
+
+/* Copy n host doubles of problem parameters (see enum irk_problem). */
+int irk_set_params(irk_ctx *ctx, const double *host_params, int n);
+
+int irk_set_option(irk_ctx *ctx, int key, int64_t val);
+
+/* Bytes of caller-owned DEVICE workspace irk_integrate needs.  Layout: a
+ * 64-byte header {int64 n_done, ...}, then the history L_{n-1} [8][dim][batch]
+ * fp64, then per-trajectory stats [4][batch] int64 {maxiter_hits, diverged_step
+ * (1-based absolute step, 0 = none), sweeps_total, reserved}.  A zero-filled workspace means "first
+ * step" (zero history, n_done = 0); reusing it continues the integration bitwise
+ * as if uninterrupted (t_{n-1} = t0 + (n-1) h with the absolute n). */
+size_t irk_workspace_bytes(const irk_ctx *ctx);
+
+/* Advance y (device, [dim][batch]) by nsteps steps.  t0 is the initial time of
+ * the whole run.  energy (device, [(nsteps/E)+1][batch]) receives H(y) at local
+ * steps 0, E, 2E, ... when ENERGY_EVERY = E > 0, else may be NULL.  iters
+ * (device, [batch]) receives the number of fixed-point sweeps of this call per
+ * trajectory, or NULL. */
+int irk_integrate(irk_ctx *ctx, double *y, double t0, void *workspace, double *energy,
+                  int64_t *iters, void *stream);
+
+/* Same, end to end from HOST memory: copies y_host (pinned or pageable) to an
+ * internal device buffer, integrates from a fresh (zero) internal workspace,
+ * copies the result back into y_host and, if non-NULL, energy_host / iters_host;
+ * synchronises `stream` before returning. */
+int irk_integrate_host(irk_ctx *ctx, double *y_host, double t0, double *energy_host,
+                       int64_t *iters_host, void *stream);
+
+/* H(y) per trajectory (device in, device out [batch]); Neumaier-compensated,
+ * canonical term order. */
+int irk_energy(irk_ctx *ctx, const double *y, double *H, void *stream);
+
+/* Synchronises `stream`, reduces the workspace stats: out = {trajectories with
+ * MAX_ITERS hits, diverged trajectories, first diverged step (-1), total sweeps}.
+ * Returns IRK_E_DIVERGED, IRK_W_MAXITER or IRK_OK accordingly. */
+int irk_stats(irk_ctx *ctx, const void *workspace, void *stream, int64_t out[4]);
+
+/* Host copy of the fp64 tableau the kernels use: c~[8], b~[8], mu~[8*8], nu~[8*8]
+ * (row-major [i*8+j]).  Returns IRK_OK. */
+int irk_tableau(double *c, double *b, double *mu, double *nu);
+
+/* NCCL communicator for a body-sharded IRK_NBODY_DIRECT system: rank r of
+ * nranks owns bodies [r*N/nranks, (r+1)*N/nranks); nccl_unique_id points to a
+ * 128-byte ncclUniqueId created by rank 0 and broadcast by the caller. */
+int irk_set_comm(irk_ctx *ctx, const void *nccl_unique_id, int rank, int nranks);
+
+/* NULL ctx: the thread-local message of the last failed irk_create. */
+const char *irk_last_error(const irk_ctx *ctx);
+
+void irk_destroy(irk_ctx *ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,353 @@
+// C ABI of the IRKGL16 library (include/irk.h): context, workspace, dispatch.
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/irk.h"
+#include "ensemble_g1.cuh"
+#include "problems.cuh"
+#include "tableau.h"
+
+using irk::EnsArgs;
+using irk::Tableau;
+
+static thread_local std::string g_create_error;
+
+struct irk_ctx {
+    int problem = 0, dim = 0;
+    double h = 0.0;
+    int64_t nsteps = 0, batch = 0;
+    std::vector<double> params;
+    bool have_params = false;
+    int mode = 0, max_iters = 100, mapping = 0;
+    int64_t energy_every = 0;
+    Tableau T;
+    std::string err;
+    // buffers owned by the ctx for irk_integrate_host
+    double *d_y = nullptr, *d_energy = nullptr;
+    int64_t *d_iters = nullptr;
+    void *d_ws = nullptr;
+    size_t cap_y = 0, cap_energy = 0, cap_ws = 0;
+    int64_t cap_iters = 0;
+};
+
+namespace {
+
+constexpr size_t kHeader = 64;
+
+int fail(irk_ctx *c, int code, const char *fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    if (c) c->err = buf;
+    return code;
+}
+
+int cuda_check(irk_ctx *c, cudaError_t e, const char *what) {
+    if (e == cudaSuccess) return IRK_OK;
+    return fail(c, IRK_E_CUDA, "%s: %s", what, cudaGetErrorString(e));
+}
+
+size_t hist_bytes(const irk_ctx *c) { return sizeof(double) * 8 * (size_t)c->dim * c->batch; }
+size_t stats_bytes(const irk_ctx *c) { return sizeof(int64_t) * 4 * (size_t)c->batch; }
+
+int n_params_expected(int problem, int dim) {
+    switch (problem) {
+    case IRK_KEPLER: return 1;
+    case IRK_HENON_HEILES: return 2;
+    case IRK_FPU_BETA: return 1;
+    case IRK_NBODY:
+    case IRK_NBODY_DIRECT: return 2 + dim / 6;
+    }
+    return -1;
+}
+
+__global__ void advance_n_kernel(int64_t *n_done, int64_t nsteps) { *n_done += nsteps; }
+
+template <class P>
+int launch_g1(irk_ctx *c, const P &prob, double *y, double t0, char *ws, double *energy,
+              int64_t *iters, cudaStream_t st) {
+    EnsArgs a;
+    a.T = c->T;
+    a.y = y;
+    a.n_done = reinterpret_cast<const int64_t *>(ws);
+    a.hist = reinterpret_cast<double *>(ws + kHeader);
+    a.stats = reinterpret_cast<int64_t *>(ws + kHeader + hist_bytes(c));
+    a.energy = energy;
+    a.iters = iters;
+    a.batch = c->batch;
+    a.nsteps = c->nsteps;
+    a.energy_every = c->energy_every;
+    a.h = c->h;
+    a.t0 = t0;
+    a.max_iters = c->max_iters;
+    const int threads = 64;
+    const int64_t blocks = (c->batch + threads - 1) / threads;
+    irk::ens_g1_kernel<P><<<(unsigned)blocks, threads, 0, st>>>(a, prob);
+    return cuda_check(c, cudaGetLastError(), "ens_g1_kernel launch");
+}
+
+template <class P>
+__global__ void energy_g1_kernel(const double *y, double *H, int64_t B, const __grid_constant__ P prob) {
+    constexpr int d = P::d;
+    int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (b >= B) return;
+    double q[d], v[d];
+    for (int l = 0; l < d; ++l) {
+        q[l] = y[l * B + b];
+        v[l] = y[(d + l) * B + b];
+    }
+    H[b] = prob.energy(q, v);
+}
+
+}  // namespace
+
+extern "C" {
+
+irk_ctx *irk_create(int problem, int dim, double h, int64_t nsteps, int64_t batch) {
+    g_create_error.clear();
+    auto bad = [](const char *m) -> irk_ctx * {
+        g_create_error = m;
+        return nullptr;
+    };
+    switch (problem) {
+    case IRK_KEPLER:
+    case IRK_HENON_HEILES:
+        if (dim != 4) return bad("irk_create: Kepler/Henon-Heiles need dim == 4");
+        break;
+    case IRK_FPU_BETA:
+        if (dim < 2 || dim % 2) return bad("irk_create: FPU needs an even dim >= 2");
+        return bad("irk_create: IRK_FPU_BETA kernel not built yet");
+    case IRK_NBODY:
+    case IRK_NBODY_DIRECT:
+        if (dim % 6 || dim < 12) return bad("irk_create: N-body needs dim = 6N, N >= 2");
+        return bad("irk_create: N-body kernels not built yet");
+    default: return bad("irk_create: unknown problem");
+    }
+    if (!std::isfinite(h) || h == 0.0) return bad("irk_create: h must be finite and nonzero");
+    if (nsteps < 0) return bad("irk_create: nsteps < 0");
+    if (batch < 1) return bad("irk_create: batch < 1");
+    irk_ctx *c = new irk_ctx;
+    c->problem = problem;
+    c->dim = dim;
+    c->h = h;
+    c->nsteps = nsteps;
+    c->batch = batch;
+    char err[256];
+    if (irk::build_tableau(h, &c->T, err, sizeof err)) {
+        g_create_error = err;
+        delete c;
+        return nullptr;
+    }
+    return c;
+}
+
+int irk_set_params(irk_ctx *c, const double *p, int n) {
+    if (!c) return IRK_E_ARG;
+    if (!p || n != n_params_expected(c->problem, c->dim))
+        return fail(c, IRK_E_ARG, "irk_set_params: expected %d params", n_params_expected(c->problem, c->dim));
+    for (int i = 0; i < n; ++i)
+        if (!std::isfinite(p[i])) return fail(c, IRK_E_ARG, "irk_set_params: non-finite param %d", i);
+    c->params.assign(p, p + n);
+    c->have_params = true;
+    return IRK_OK;
+}
+
+int irk_set_option(irk_ctx *c, int key, int64_t val) {
+    if (!c) return IRK_E_ARG;
+    switch (key) {
+    case IRK_OPT_MODE:
+        if (val != 0) return fail(c, IRK_E_ARG, "irk_set_option: first-order mode not built yet");
+        c->mode = (int)val;
+        return IRK_OK;
+    case IRK_OPT_MAX_ITERS:
+        if (val < 1 || val > 1000000) return fail(c, IRK_E_ARG, "irk_set_option: MAX_ITERS out of range");
+        c->max_iters = (int)val;
+        return IRK_OK;
+    case IRK_OPT_ENERGY_EVERY:
+        if (val < 0) return fail(c, IRK_E_ARG, "irk_set_option: ENERGY_EVERY < 0");
+        c->energy_every = val;
+        return IRK_OK;
+    case IRK_OPT_MAPPING:
+        if (val < 0) return fail(c, IRK_E_ARG, "irk_set_option: bad MAPPING");
+        c->mapping = (int)val;
+        return IRK_OK;
+    }
+    return fail(c, IRK_E_ARG, "irk_set_option: unknown key %d", key);
+}
+
+size_t irk_workspace_bytes(const irk_ctx *c) {
+    if (!c) return 0;
+    return kHeader + hist_bytes(c) + stats_bytes(c);
+}
+
+int irk_integrate(irk_ctx *c, double *y, double t0, void *workspace, double *energy, int64_t *iters,
+                  void *stream) {
+    if (!c) return IRK_E_ARG;
+    if (!c->have_params) return fail(c, IRK_E_STATE, "irk_integrate: irk_set_params not called");
+    if (!y || !workspace) return fail(c, IRK_E_ARG, "irk_integrate: null y or workspace");
+    if (!std::isfinite(t0)) return fail(c, IRK_E_ARG, "irk_integrate: non-finite t0");
+    if (c->energy_every > 0 && !energy) return fail(c, IRK_E_ARG, "irk_integrate: ENERGY_EVERY set but energy == NULL");
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    char *ws = static_cast<char *>(workspace);
+    int rc;
+    switch (c->problem) {
+    case IRK_KEPLER: {
+        irk::Kepler P{c->params[0]};
+        rc = launch_g1(c, P, y, t0, ws, energy, iters, st);
+        break;
+    }
+    case IRK_HENON_HEILES: {
+        irk::HenonHeiles P{c->params[0], c->params[1]};
+        rc = launch_g1(c, P, y, t0, ws, energy, iters, st);
+        break;
+    }
+    default: return fail(c, IRK_E_ARG, "irk_integrate: problem not supported");
+    }
+    if (rc) return rc;
+    advance_n_kernel<<<1, 1, 0, st>>>(reinterpret_cast<int64_t *>(ws), c->nsteps);
+    return cuda_check(c, cudaGetLastError(), "advance_n launch");
+}
+
+int irk_integrate_host(irk_ctx *c, double *y_host, double t0, double *energy_host, int64_t *iters_host,
+                       void *stream) {
+    if (!c) return IRK_E_ARG;
+    if (!y_host) return fail(c, IRK_E_ARG, "irk_integrate_host: null y");
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    const size_t ybytes = sizeof(double) * (size_t)c->dim * c->batch;
+    const size_t wsb = irk_workspace_bytes(c);
+    const size_t ebytes = c->energy_every > 0 ? sizeof(double) * (size_t)(c->nsteps / c->energy_every + 1) * c->batch : 0;
+    int rc;
+    if (c->cap_y < ybytes) {
+        cudaFree(c->d_y);
+        c->d_y = nullptr;
+        c->cap_y = 0;
+        if ((rc = cuda_check(c, cudaMalloc(&c->d_y, ybytes), "cudaMalloc y"))) return rc;
+        c->cap_y = ybytes;
+    }
+    if (c->cap_ws < wsb) {
+        cudaFree(c->d_ws);
+        c->d_ws = nullptr;
+        c->cap_ws = 0;
+        if ((rc = cuda_check(c, cudaMalloc(&c->d_ws, wsb), "cudaMalloc workspace"))) return rc;
+        c->cap_ws = wsb;
+    }
+    if (ebytes && c->cap_energy < ebytes) {
+        cudaFree(c->d_energy);
+        c->d_energy = nullptr;
+        c->cap_energy = 0;
+        if ((rc = cuda_check(c, cudaMalloc(&c->d_energy, ebytes), "cudaMalloc energy"))) return rc;
+        c->cap_energy = ebytes;
+    }
+    if (iters_host && c->cap_iters < c->batch) {
+        cudaFree(c->d_iters);
+        c->d_iters = nullptr;
+        c->cap_iters = 0;
+        if ((rc = cuda_check(c, cudaMalloc(&c->d_iters, sizeof(int64_t) * c->batch), "cudaMalloc iters"))) return rc;
+        c->cap_iters = c->batch;
+    }
+    if ((rc = cuda_check(c, cudaMemcpyAsync(c->d_y, y_host, ybytes, cudaMemcpyHostToDevice, st), "H2D y"))) return rc;
+    if ((rc = cuda_check(c, cudaMemsetAsync(c->d_ws, 0, wsb, st), "memset workspace"))) return rc;
+    if ((rc = irk_integrate(c, c->d_y, t0, c->d_ws, ebytes ? c->d_energy : nullptr,
+                            iters_host ? c->d_iters : nullptr, stream)))
+        return rc;
+    if ((rc = cuda_check(c, cudaMemcpyAsync(y_host, c->d_y, ybytes, cudaMemcpyDeviceToHost, st), "D2H y"))) return rc;
+    if (energy_host && ebytes &&
+        (rc = cuda_check(c, cudaMemcpyAsync(energy_host, c->d_energy, ebytes, cudaMemcpyDeviceToHost, st), "D2H energy")))
+        return rc;
+    if (iters_host &&
+        (rc = cuda_check(c, cudaMemcpyAsync(iters_host, c->d_iters, sizeof(int64_t) * c->batch, cudaMemcpyDeviceToHost, st),
+                         "D2H iters")))
+        return rc;
+    return cuda_check(c, cudaStreamSynchronize(st), "irk_integrate_host sync");
+}
+
+int irk_energy(irk_ctx *c, const double *y, double *H, void *stream) {
+    if (!c) return IRK_E_ARG;
+    if (!c->have_params) return fail(c, IRK_E_STATE, "irk_energy: irk_set_params not called");
+    if (!y || !H) return fail(c, IRK_E_ARG, "irk_energy: null pointer");
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    const int threads = 128;
+    const unsigned blocks = (unsigned)((c->batch + threads - 1) / threads);
+    switch (c->problem) {
+    case IRK_KEPLER:
+        energy_g1_kernel<<<blocks, threads, 0, st>>>(y, H, c->batch, irk::Kepler{c->params[0]});
+        break;
+    case IRK_HENON_HEILES:
+        energy_g1_kernel<<<blocks, threads, 0, st>>>(y, H, c->batch, irk::HenonHeiles{c->params[0], c->params[1]});
+        break;
+    default: return fail(c, IRK_E_ARG, "irk_energy: problem not supported");
+    }
+    return cuda_check(c, cudaGetLastError(), "energy kernel launch");
+}
+
+int irk_stats(irk_ctx *c, const void *workspace, void *stream, int64_t out[4]) {
+    if (!c || !workspace || !out) return IRK_E_ARG;
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    std::vector<int64_t> s(4 * (size_t)c->batch);
+    int rc = cuda_check(c,
+                        cudaMemcpyAsync(s.data(), static_cast<const char *>(workspace) + kHeader + hist_bytes(c),
+                                        stats_bytes(c), cudaMemcpyDeviceToHost, st),
+                        "D2H stats");
+    if (rc) return rc;
+    if ((rc = cuda_check(c, cudaStreamSynchronize(st), "irk_stats sync"))) return rc;
+    int64_t hit_traj = 0, div_traj = 0, first_bad = -1, total = 0;
+    const int64_t B = c->batch;
+    for (int64_t b = 0; b < B; ++b) {
+        if (s[b] > 0) ++hit_traj;
+        if (s[B + b] > 0) {  // diverged_step is 1-based; 0 = none
+            ++div_traj;
+            if (first_bad < 0 || s[B + b] < first_bad) first_bad = s[B + b];
+        }
+        total += s[2 * B + b];
+    }
+    out[0] = hit_traj;
+    out[1] = div_traj;
+    out[2] = first_bad;
+    out[3] = total;
+    if (div_traj) return IRK_E_DIVERGED;
+    if (hit_traj) return IRK_W_MAXITER;
+    return IRK_OK;
+}
+
+int irk_tableau(double *c, double *b, double *mu, double *nu) {
+    Tableau T;
+    char err[256];
+    if (irk::build_tableau(1.0, &T, err, sizeof err)) return IRK_E_ARG;
+    if (c) memcpy(c, T.c, sizeof T.c);
+    if (b) memcpy(b, T.b, sizeof T.b);
+    if (mu) memcpy(mu, T.mu, sizeof T.mu);
+    if (nu) memcpy(nu, T.nu, sizeof T.nu);
+    return IRK_OK;
+}
+
+int irk_set_comm(irk_ctx *c, const void *id, int rank, int nranks) {
+    if (!c) return IRK_E_ARG;
+    (void)id;
+    (void)rank;
+    (void)nranks;
+    return fail(c, IRK_E_STATE, "irk_set_comm: body-sharded N-body not built yet");
+}
+
+const char *irk_last_error(const irk_ctx *c) {
+    if (!c) return g_create_error.c_str();
+    return c->err.c_str();
+}
+
+void irk_destroy(irk_ctx *c) {
+    if (!c) return;
+    cudaFree(c->d_y);
+    cudaFree(c->d_energy);
+    cudaFree(c->d_iters);
+    cudaFree(c->d_ws);
+    delete c;
+}
+
+}  // extern "C"

@@ -1,0 +1,31 @@
+// FP64 FMA-pipe throughput probe (include/irk_probe.h).
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "../../include/irk_probe.h"
+
+namespace {
+__global__ void __launch_bounds__(256) dfma_probe_kernel(double *out, int iters) {
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    double x = 1.0 + 1e-9 * t, y = 1.0 - 1e-12 * t;
+    double acc[16];
+#pragma unroll
+    for (int k = 0; k < 16; ++k) acc[k] = 1e-3 * (k + 1);
+    for (int i = 0; i < iters; ++i) {
+#pragma unroll
+        for (int k = 0; k < 16; ++k) acc[k] = __fma_rn(acc[k], x, y);
+    }
+    double s = 0.0;
+#pragma unroll
+    for (int k = 0; k < 16; ++k) s += acc[k];
+    out[t] = s;
+}
+}  // namespace
+
+extern "C" int64_t irk_probe_dfma(double *out, int blocks, int iters, void *stream) {
+    if (!out || blocks < 1 || iters < 1) return -1;
+    dfma_probe_kernel<<<blocks, 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(out, iters);
+    if (cudaGetLastError() != cudaSuccess) return -1;
+    return (int64_t)blocks * 256 * iters * 16 * 2;
+}

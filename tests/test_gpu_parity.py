@@ -1,0 +1,184 @@
+"""GPU parity: the CUDA path (through the C ABI) against the scalar-C oracle on
+the same seeded inputs.
+
+The bar: both sides execute the same IEEE operation
+sequence, so states, sweep counts and energy samples must be BITWISE equal;
+the north-star tolerances (max relative state error <= 1e-10, |dH_gpu - dH_orc|
+<= 1e-13) are asserted as well so a failure report says by how much.
+"""
+import math
+
+import numpy as np
+import pytest
+
+from paper_2511_03655_b200 import workloads as wl
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("no CUDA device", allow_module_level=True)
+
+
+@pytest.fixture(scope="module")
+def irk():
+    from paper_2511_03655_b200 import build, irk
+    build.build()
+    return irk
+
+
+def run_gpu(irk, w, y=None, nsteps=None, energy_every=0, max_iters=100, chunks=1, t0=0.0):
+    y = w.y if y is None else y
+    nsteps = w.nsteps if nsteps is None else nsteps
+    assert nsteps % chunks == 0
+    per = nsteps // chunks
+    B = y.shape[1]
+    with irk.Integrator(w.problem, w.dim, w.h, per, B, w.params, energy_every=energy_every,
+                        max_iters=max_iters) as ig:
+        Y = torch.tensor(y, dtype=torch.float64, device="cuda").contiguous()
+        ws = ig.new_workspace()
+        it_total = torch.zeros(B, dtype=torch.int64, device="cuda")
+        it = torch.zeros(B, dtype=torch.int64, device="cuda")
+        E = (torch.zeros((ig.n_energy(), B), dtype=torch.float64, device="cuda")
+             if energy_every else None)
+        Es = []
+        for _ in range(chunks):
+            ig.integrate(Y, ws, t0=t0, energy=E, iters=it)
+            it_total += it
+            if E is not None:
+                Es.append(E.cpu().numpy().copy())
+        torch.cuda.synchronize()
+        rc, st = ig.stats(ws)
+        return dict(y=Y.cpu().numpy(), iters=it_total.cpu().numpy(),
+                    energy=(np.concatenate([Es[0]] + [e[1:] for e in Es[1:]]) if Es else None),
+                    rc=rc, stats=st, hist=ig.hist_view(ws).cpu().numpy())
+
+
+def assert_parity(g, o, energy=False):
+    yg, yo = g["y"], o["y"] if o["y"].ndim == 2 else o["y"][:, None]
+    scale = np.maximum(np.abs(yo).max(axis=0), 1e-300)
+    rel = (np.abs(yg - yo).max(axis=0) / scale).max()
+    assert rel <= 1e-10, f"max relative state error {rel:.3e}"
+    if energy:
+        eg, eo = g["energy"], o["energy"]
+        dg = (eg - eg[0]) / eg[0]
+        do = (eo - eo[0]) / eo[0]
+        assert np.abs(dg - do).max() <= 1e-13
+        assert np.array_equal(eg, eo), "energy samples not bitwise equal"
+    nbad = int((yg != yo).any(axis=0).sum())
+    assert nbad == 0, f"{nbad} trajectories not bitwise equal (max rel {rel:.3e})"
+    assert np.array_equal(g["iters"], o["iters"]), "sweep counts differ"
+
+
+def test_config1_kepler_single_full(irk, orc):
+    """Config 1 in full: 12,800 steps, energy every 128 steps, bitwise."""
+    w = wl.kepler_single()
+    g = run_gpu(irk, w, energy_every=128)
+    o = orc.integrate(w.problem, w.y, w.params, w.h, w.nsteps, energy_every=128)
+    assert_parity(g, o, energy=True)
+    assert g["rc"] == irk.OK
+
+
+def test_config2_ragged_subset_full_length(irk, orc):
+    """Config 2 generator, a ragged batch (1000 = not a multiple of the block),
+    full 10,000 steps, energy samples every 500 steps, bitwise."""
+    w = wl.kepler_ensemble(batch=1000)
+    g = run_gpu(irk, w, energy_every=500)
+    o = orc.integrate(w.problem, w.y, w.params, w.h, w.nsteps, energy_every=500)
+    assert_parity(g, o, energy=True)
+
+
+def test_config2_full_batch_sampled(irk, orc):
+    """Config 2 at full size (65,536 x 10,000) in the launch configuration the
+    bench times; the oracle recomputes a sample of 192 trajectories spread over
+    the batch plus the 64 most eccentric (hardest) ones."""
+    w = wl.kepler_ensemble()
+    g = run_gpu(irk, w)
+    e = w.meta["e"]
+    idx = np.unique(np.concatenate([np.linspace(0, w.batch - 1, 192).astype(int),
+                                    np.argsort(e)[-64:]]))
+    o = orc.integrate(w.problem, w.y[:, idx], w.params, w.h, w.nsteps)
+    sub = dict(y=g["y"][:, idx], iters=g["iters"][idx])
+    assert_parity(sub, o)
+    assert g["stats"]["diverged_traj"] == 0
+
+
+def test_chunked_calls_continue_bitwise(irk, orc):
+    """Workspace (history + n) carries the state: 4 chunks == one oracle run."""
+    w = wl.kepler_ensemble(batch=130, nsteps=400)
+    g = run_gpu(irk, w, chunks=4)
+    o = orc.integrate(w.problem, w.y, w.params, w.h, w.nsteps)
+    assert_parity(g, o)
+    oh = o["hist"].transpose(1, 2, 0)  # (batch, 8, dim) -> (8, dim, batch)
+    assert np.array_equal(g["hist"], oh)
+
+
+def test_henon_heiles_parity(irk, orc):
+    w = wl.henon_heiles(batch=300, nsteps=2000)
+    g = run_gpu(irk, w, energy_every=100)
+    o = orc.integrate(w.problem, w.y, w.params, w.h, w.nsteps, energy_every=100)
+    assert_parity(g, o, energy=True)
+
+
+def test_henon_heiles_time_dependent_close(irk, orc):
+    """xi != 0 uses sin(t): CUDA's sin and libm's differ in the last ulp, so this
+    case is compared at the north-star tolerance only (R-7)."""
+    w = wl.henon_heiles(batch=64, nsteps=500, xi=0.1, lam=1.0)
+    g = run_gpu(irk, w, t0=0.25)
+    o = orc.integrate(w.problem, w.y, w.params, w.h, w.nsteps, t0=0.25)
+    rel = (np.abs(g["y"] - o["y"]).max(axis=0) / np.abs(o["y"]).max(axis=0)).max()
+    assert rel <= 1e-10
+
+
+def test_max_iters_cap_flagged_like_oracle(irk, orc):
+    w = wl.kepler_ensemble(batch=70, nsteps=50)
+    g = run_gpu(irk, w, max_iters=3)
+    o = orc.integrate(w.problem, w.y, w.params, w.h, w.nsteps, max_iters=3)
+    assert_parity(g, o)
+    assert g["rc"] == irk.W_MAXITER
+    assert g["stats"]["maxiter_traj"] == int((o["status"][:, 0] > 0).sum())
+
+
+def test_negative_h_reversibility(irk, orc):
+    w = wl.kepler_ensemble(batch=65, nsteps=64)
+    g1 = run_gpu(irk, w)
+    wb = wl.Workload(w.name, w.problem, w.dim, g1["y"], w.params, -w.h, 64)
+    g2 = run_gpu(irk, wb)
+    o2 = orc.integrate(w.problem, g1["y"], w.params, -w.h, 64)
+    assert_parity(g2, o2)
+    assert np.abs(g2["y"] - w.y).max() < 1e-12
+
+
+def test_divergence_flag_and_freeze(irk, orc):
+    y = np.array([[1e-200, 1.0, 0.5], [0.0, 0.0, 0.0], [0.0, 0.0, 0.0], [0.0, 1.0, 1.0]])
+    w = wl.Workload("div", wl.KEPLER, 4, y, np.array([1.0]), 0.1, 20)
+    g = run_gpu(irk, w)
+    o = orc.integrate(w.problem, y, w.params, w.h, 20)
+    assert g["rc"] == irk.E_DIVERGED
+    assert g["stats"]["diverged_traj"] == 1
+    assert g["stats"]["first_bad_step"] == o["status"][0, 1]
+    np.testing.assert_array_equal(g["y"][:, 1:], o["y"][:, 1:])
+
+
+def test_zero_steps_and_batch_one(irk):
+    w = wl.kepler_single()
+    g = run_gpu(irk, w, nsteps=0)
+    assert np.array_equal(g["y"], w.y) and g["iters"][0] == 0
+
+
+def test_energy_entry_point_matches_oracle(irk, orc):
+    w = wl.kepler_ensemble(batch=257)
+    with irk.Integrator(w.problem, w.dim, w.h, 1, w.batch, w.params) as ig:
+        H = ig.energy(torch.tensor(w.y, device="cuda")).cpu().numpy()
+    Ho = np.array([orc.energy(w.problem, 4, w.params, w.y[:, b]) for b in range(w.batch)])
+    assert np.array_equal(H, Ho)
+
+
+def test_integrate_host_end_to_end(irk, orc):
+    w = wl.kepler_ensemble(batch=100, nsteps=200)
+    with irk.Integrator(w.problem, w.dim, w.h, w.nsteps, w.batch, w.params, energy_every=50) as ig:
+        y = np.ascontiguousarray(w.y.copy())
+        E, it = ig.integrate_host(y)
+    o = orc.integrate(w.problem, w.y, w.params, w.h, w.nsteps, energy_every=50)
+    assert np.array_equal(y, o["y"]) and np.array_equal(it, o["iters"])
+    assert np.array_equal(E, o["energy"])

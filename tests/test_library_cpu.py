@@ -1,0 +1,94 @@
+"""Host-side checks of the C-ABI library (no GPU): the .so loads and exports
+every symbol include/irk.h declares; the library's own tableau (Newton +
+Bjorck-Pereyra in __float128) equals, bit for bit, the oracle's independently
+computed one and the mpmath round-to-nearest values; argument errors are
+reported synchronously by irk_create / irk_set_params / irk_set_option.
+"""
+import ctypes
+import math
+import os
+import re
+
+import mpmath as mp
+import numpy as np
+import pytest
+
+from tests import mp_tableau
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module")
+def irk():
+    from paper_2511_03655_b200 import build, irk
+    build.build()
+    return irk
+
+
+def declared_symbols():
+    names = []
+    for f in os.listdir(os.path.join(ROOT, "include")):
+        if f.endswith(".h"):
+            src = open(os.path.join(ROOT, "include", f)).read()
+            names += re.findall(r"^\s*(?:const\s+)?[a-zA-Z_][\w\s\*]*?\b(irk_\w+)\s*\(", src, re.M)
+    return sorted(set(names))
+
+
+def test_exports_every_declared_symbol(irk):
+    names = declared_symbols()
+    assert len(names) >= 12
+    lib = ctypes.CDLL(irk.LIB_PATH)
+    for n in names:
+        assert hasattr(lib, n), n
+    assert set(names) == set(irk.SYMBOLS)
+
+
+def test_library_tableau_bitwise_equals_oracle_and_mpmath(irk, orc):
+    c, b, mu, nu = irk.tableau()
+    oc, ob, omu, onu = orc.tableau(8)
+    assert np.array_equal(c, oc) and np.array_equal(b, ob)
+    assert np.array_equal(mu, omu) and np.array_equal(nu, onu)
+    c_mp, b_mp, a_mp, nu_mp = mp_tableau.tableau(8)
+    for i in range(8):
+        assert c[i] == mp_tableau.rn(c_mp[i])
+        for j in range(i):
+            assert mu[i, j] == mp_tableau.rn(a_mp[i][j] / b_mp[j])
+
+
+@pytest.mark.parametrize("args", [
+    (1, 6, 0.1, 10, 4),          # Kepler needs dim 4
+    (4, 4, 0.0, 10, 4),          # h = 0
+    (1, 4, float("nan"), 10, 4),
+    (1, 4, 0.1, -1, 4),          # nsteps < 0
+    (1, 4, 0.1, 10, 0),          # batch < 1
+    (9, 4, 0.1, 10, 4),          # unknown problem
+    (2, 13, 0.1, 10, 4),         # N-body dim % 6
+    (3, 7, 0.1, 10, 4),          # FPU odd dim
+])
+def test_create_argument_errors(irk, args):
+    with pytest.raises(irk.IrkError):
+        irk.Integrator(*args, params=[1.0])
+
+
+def test_params_and_options_errors(irk):
+    with pytest.raises(irk.IrkError):
+        irk.Integrator(irk.KEPLER, 4, 0.1, 10, 4, params=[1.0, 2.0])
+    with pytest.raises(irk.IrkError):
+        irk.Integrator(irk.KEPLER, 4, 0.1, 10, 4, params=[float("inf")])
+    with pytest.raises(irk.IrkError):
+        irk.Integrator(irk.KEPLER, 4, 0.1, 10, 4, params=[1.0], max_iters=0)
+    w = irk.Integrator(irk.KEPLER, 4, -0.1, 10, 4, params=[1.0])  # negative h is allowed
+    assert w.workspace_bytes == 64 + 8 * 8 * 4 * 4 + 8 * 4 * 4
+    w.close()
+
+
+def test_build_is_sm100a_only(irk):
+    """The library carries sm_100a SASS (cuobjdump) and nothing for other archs."""
+    import shutil
+    import subprocess
+    exe = shutil.which("cuobjdump") or "/usr/local/cuda/bin/cuobjdump"
+    if not os.path.exists(exe):
+        pytest.skip("cuobjdump not available")
+    out = subprocess.run([exe, "--list-elf", irk.LIB_PATH], capture_output=True, text=True).stdout
+    archs = set(re.findall(r"sm_(\d+a?)", out))
+    assert archs == {"100a"}, archs
