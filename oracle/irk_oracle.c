@@ -497,9 +497,11 @@ static int step_partitioned(const orc_cfg *cfg, const coef_t *K, double tn1, dou
         q[l] = q[l] + sum8(&w->Lq[l], d);
         v[l] = v[l] + sum8(&w->Lv[l], d);
     }
+    /* the partitioned history is L^v only (Eq. IRK_init2 extrapolates velocities);
+     * the q block is zeroed (R-4) */
     for (int j = 0; j < S8; ++j)
         for (int l = 0; l < d; ++l) {
-            hist[j * D + l] = w->Lq[j * d + l];
+            hist[j * D + l] = 0.0;
             hist[j * D + d + l] = w->Lv[j * d + l];
         }
     return k;

@@ -25,8 +25,15 @@
 
 namespace irk {
 
+// mu~, nu~ and c~ do not depend on h: one copy per device in the constant bank
+// (uploaded once per device by irk_api.cu), read as uniform operands.  hb~ =
+// fl(h b~) depends on h and travels in the kernel parameters.
+__constant__ double c_mu[8][8];
+__constant__ double c_nu[8][8];
+__constant__ double c_c[8];
+
 struct EnsArgs {
-    Tableau T;
+    double hb[8];
     double *y;            // [dim][batch]
     double *hist;         // [8][dim][batch]
     int64_t *stats;       // [4][batch]
@@ -38,17 +45,28 @@ struct EnsArgs {
     int max_iters;
 };
 
+constexpr int G1_THREADS = 64;
+
 template <class P>
-__global__ void __launch_bounds__(64, 8) ens_g1_kernel(const __grid_constant__ EnsArgs a,
+__global__ void __launch_bounds__(G1_THREADS, 8) ens_g1_kernel(const __grid_constant__ EnsArgs a,
                                                     const __grid_constant__ P prob) {
     constexpr int d = P::d, D = 2 * d;
     const int64_t B = a.batch;
     const int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    __shared__ __align__(16) double sW[2][64];  // [0] = mu~, [1] = nu~ (row-major)
+    for (int e = threadIdx.x; e < 128; e += blockDim.x) sW[e >> 6][e & 63] = (e < 64) ? (&c_mu[0][0])[e] : (&c_nu[0][0])[e - 64];
+    __syncthreads();
     if (b >= B) return;
 
     int64_t bad = a.stats[1 * B + b];
     int64_t hits = 0, sweeps = 0;
-    double q[d], v[d], V[8][d], Q[8][d], Lq[8][d], m[d], p[d];
+    // Q^[k-1] (only compared against, once per sweep) and the stop-test history
+    // (m, p) live in shared memory, [element][thread] so that the 64-bit accesses
+    // of a warp hit 32 distinct banks; registers are kept for V, the fresh Q^[k]
+    // and the RHS temporaries (ILP across the eight stages).
+    __shared__ double sQ[8 * d][G1_THREADS], sL[8 * d][G1_THREADS], sM[d][G1_THREADS], sP[d][G1_THREADS];
+    const int tx = threadIdx.x;
+    double q[d], v[d], V[8][d];
 #pragma unroll
     for (int l = 0; l < d; ++l) {
         q[l] = a.y[l * B + b];
@@ -71,72 +89,115 @@ __global__ void __launch_bounds__(64, 8) ens_g1_kernel(const __grid_constant__ E
         for (int i = 0; i < 8; ++i)
 #pragma unroll
             for (int l = 0; l < d; ++l) {
-                double acc = dmul(a.T.nu[i][0], H[0][l]);
+                double acc = dmul(c_nu[i][0], H[0][l]);
 #pragma unroll
-                for (int j = 1; j < 8; ++j) acc = dfma(a.T.nu[i][j], H[j][l], acc);
+                for (int j = 1; j < 8; ++j) acc = dfma(c_nu[i][j], H[j][l], acc);
                 V[i][l] = dadd(v[l], acc);
             }
     }
+    const double kInf = __longlong_as_double(0x7ff0000000000000LL);
 #pragma unroll
-    for (int l = 0; l < d; ++l) {
-        m[l] = p[l] = __longlong_as_double(0x7ff0000000000000LL);
-#pragma unroll
-        for (int i = 0; i < 8; ++i) Q[i][l] = 0.0;  // Q^[0] is never compared (R2)
-    }
+    for (int l = 0; l < d; ++l) sM[l][tx] = sP[l][tx] = kInf;
 
     int64_t n = 0;
     int k = 0;
     while (n < a.nsteps) {
         ++k;
-        // a2: Lq_j = hb_j V_j ; Q_i^[k] = q + D(mu_i., Lq)   (+ a5 on the fly)
+        // a2: Lq_j = hb_j V_j ; Q_i^[k] = q + D(mu_i., Lq)   (+ a5 on the fly).
+        // S(Lq) is formed here (same left-to-right order as the update needs) so
+        // that Lq dies before the RHS: 16 fewer live doubles across a3.
+        double Lq[8][d], sLq[d];
 #pragma unroll
         for (int j = 0; j < 8; ++j)
 #pragma unroll
-            for (int l = 0; l < d; ++l) Lq[j][l] = dmul(a.T.hb[j], V[j][l]);
-        bool stop = (k >= 2);
+            for (int l = 0; l < d; ++l) Lq[j][l] = dmul(a.hb[j], V[j][l]);
 #pragma unroll
         for (int l = 0; l < d; ++l) {
-            double delta = 0.0;
+            sLq[l] = Lq[0][l];
+#pragma unroll
+            for (int j = 1; j < 8; ++j) sLq[l] = dadd(sLq[l], Lq[j][l]);
+        }
+        bool stop = (k >= 2);
+        double delta[d];
+#pragma unroll
+        for (int l = 0; l < d; ++l) delta[l] = 0.0;
+        {
+            const double2 *M = reinterpret_cast<const double2 *>(&c_mu[0][0]);
 #pragma unroll
             for (int i = 0; i < 8; ++i) {
-                double acc = dmul(a.T.mu[i][0], Lq[0][l]);
+                double2 w[4];
 #pragma unroll
-                for (int j = 1; j < 8; ++j) acc = dfma(a.T.mu[i][j], Lq[j][l], acc);
-                double qn = dadd(q[l], acc);
-                double e = dabs(dsub(qn, Q[i][l]));
-                delta = (e > delta) ? e : delta;
-                Q[i][l] = qn;
+                for (int jj = 0; jj < 4; ++jj) w[jj] = M[i * 4 + jj];
+#pragma unroll
+                for (int l = 0; l < d; ++l) {
+                    double acc = dmul(w[0].x, Lq[0][l]);
+                    acc = dfma(w[0].y, Lq[1][l], acc);
+#pragma unroll
+                    for (int jj = 1; jj < 4; ++jj) {
+                        acc = dfma(w[jj].x, Lq[2 * jj][l], acc);
+                        acc = dfma(w[jj].y, Lq[2 * jj + 1][l], acc);
+                    }
+                    const double qn = dadd(q[l], acc);
+                    const double e = dabs(dsub(qn, sQ[i * d + l][tx]));  // garbage at k = 1, unused
+                    delta[l] = (e > delta[l]) ? e : delta[l];
+                    sQ[i * d + l][tx] = qn;
+                }
             }
-            if (k >= 2) {  // a5, reading R2: Delta^[k] exists from k = 2
-                double mn = (delta < p[l]) ? delta : p[l];
-                bool ok = (delta == 0.0) || (m[l] <= mn);
-                m[l] = (p[l] < m[l]) ? p[l] : m[l];
-                p[l] = delta;
+        }
+        if (k >= 2) {  // a5, reading R2: Delta^[k] exists from k = 2
+#pragma unroll
+            for (int l = 0; l < d; ++l) {
+                const double pl = sP[l][tx], ml = sM[l][tx];
+                const double mn = (delta[l] < pl) ? delta[l] : pl;
+                const bool ok = (delta[l] == 0.0) || (ml <= mn);
+                sM[l][tx] = (pl < ml) ? pl : ml;
+                sP[l][tx] = delta[l];
                 stop = stop && ok;
             }
         }
-        // a3 + a4 (first half): F_i = g(Q_i, t_i) ; Lv_i = hb_i F_i
+        // a3 + a4 (first half): F_i = g(Q_i, t_i) ; Lv_i = hb_i F_i, two stages per trip
+        // (enough ILP for the branch-free div/sqrt chains without spilling).
         const double tn1 = dadd(a.t0, dmul((double)(n0 + n), a.h));
+        {
+            bool ok = true;
+#pragma unroll 1
+            for (int i0 = 0; i0 < 8; i0 += 2) {
+#pragma unroll
+                for (int i = i0; i < i0 + 2; ++i) {
+                    double Qi[d], Fi[d];
+#pragma unroll
+                    for (int l = 0; l < d; ++l) Qi[l] = sQ[i * d + l][tx];
+                    prob.template accel<false>(Qi, Fi, dadd(tn1, dmul(c_c[i], a.h)), ok);
+#pragma unroll
+                    for (int l = 0; l < d; ++l) sL[i * d + l][tx] = dmul(a.hb[i], Fi[l]);
+                }
+            }
+            if (!ok) {  // some stage needs the exact slow path of div/sqrt: redo all, same bits
+#pragma unroll 1
+                for (int i = 0; i < 8; ++i) {
+                    double Qi[d], Fi[d];
+#pragma unroll
+                    for (int l = 0; l < d; ++l) Qi[l] = sQ[i * d + l][tx];
+                    prob.template accel<true>(Qi, Fi, dadd(tn1, dmul(c_c[i], a.h)), ok);
+#pragma unroll
+                    for (int l = 0; l < d; ++l) sL[i * d + l][tx] = dmul(a.hb[i], Fi[l]);
+                }
+            }
+        }
         double Lv[8][d];
 #pragma unroll
-        for (int i = 0; i < 8; ++i) {
-            double F[d];
-            prob.accel(Q[i], F, dadd(tn1, dmul(a.T.c[i], a.h)));
+        for (int i = 0; i < 8; ++i)
 #pragma unroll
-            for (int l = 0; l < d; ++l) Lv[i][l] = dmul(a.T.hb[i], F[l]);
-        }
+            for (int l = 0; l < d; ++l) Lv[i][l] = sL[i * d + l][tx];
         const bool fin = stop || (k >= a.max_iters);
         if (fin) {  // a6: update with the last iteration's L, history <- Lv
             bool finite = true;
 #pragma unroll
             for (int l = 0; l < d; ++l) {
-                double sq = Lq[0][l], sv = Lv[0][l];
+                double sv = Lv[0][l];
 #pragma unroll
-                for (int j = 1; j < 8; ++j) {
-                    sq = dadd(sq, Lq[j][l]);
-                    sv = dadd(sv, Lv[j][l]);
-                }
-                q[l] = dadd(q[l], sq);
+                for (int j = 1; j < 8; ++j) sv = dadd(sv, Lv[j][l]);
+                q[l] = dadd(q[l], sLq[l]);
                 v[l] = dadd(v[l], sv);
                 finite = finite && isfinite(q[l]) && isfinite(v[l]);
             }
@@ -145,31 +206,46 @@ __global__ void __launch_bounds__(64, 8) ens_g1_kernel(const __grid_constant__ E
             hits += stop ? 0 : 1;
             k = 0;
 #pragma unroll
-            for (int l = 0; l < d; ++l) m[l] = p[l] = __longlong_as_double(0x7ff0000000000000LL);
+            for (int l = 0; l < d; ++l) sM[l][tx] = sP[l][tx] = kInf;
             if (sample && (n % a.energy_every) == 0)
                 a.energy[(n / a.energy_every) * B + b] = prob.energy(q, v);
-            if (n == a.nsteps || !finite) {
+            if (n == a.nsteps || !finite) {  // history = Lv (Eq. IRK_init2 extrapolates only
+                                             // velocities); the q block is zeroed (R-4)
 #pragma unroll
                 for (int j = 0; j < 8; ++j)
 #pragma unroll
                     for (int l = 0; l < d; ++l) {
-                        a.hist[((int64_t)j * D + l) * B + b] = Lq[j][l];
+                        a.hist[((int64_t)j * D + l) * B + b] = 0.0;
                         a.hist[((int64_t)j * D + d + l) * B + b] = Lv[j][l];
                     }
                 if (!finite) bad = n0 + n;
                 break;
             }
         }
-        // a4 (second half) / next step's a1: V_i = v + D(W_i., Lv), W = fin ? nu : mu
+        // a4 (second half) / next step's a1: V_i = v + D(W_i., Lv), W = fin ? nu : mu.
+        // Lanes of a warp disagree on `fin` almost every sweep, so W is read from a
+        // shared-memory copy of both tables (two broadcast addresses per LDS.128)
+        // instead of per-coefficient selects.
+        {
+            const double2 *W = reinterpret_cast<const double2 *>(&sW[fin ? 1 : 0][0]);
 #pragma unroll
-        for (int i = 0; i < 8; ++i)
+            for (int i = 0; i < 8; ++i) {
+                double2 w[4];
 #pragma unroll
-            for (int l = 0; l < d; ++l) {
-                double acc = dmul(fin ? a.T.nu[i][0] : a.T.mu[i][0], Lv[0][l]);
+                for (int jj = 0; jj < 4; ++jj) w[jj] = W[i * 4 + jj];
 #pragma unroll
-                for (int j = 1; j < 8; ++j) acc = dfma(fin ? a.T.nu[i][j] : a.T.mu[i][j], Lv[j][l], acc);
-                V[i][l] = dadd(v[l], acc);
+                for (int l = 0; l < d; ++l) {
+                    double acc = dmul(w[0].x, Lv[0][l]);
+                    acc = dfma(w[0].y, Lv[1][l], acc);
+#pragma unroll
+                    for (int jj = 1; jj < 4; ++jj) {
+                        acc = dfma(w[jj].x, Lv[2 * jj][l], acc);
+                        acc = dfma(w[jj].y, Lv[2 * jj + 1][l], acc);
+                    }
+                    V[i][l] = dadd(v[l], acc);
+                }
             }
+        }
     }
 #pragma unroll
     for (int l = 0; l < d; ++l) {

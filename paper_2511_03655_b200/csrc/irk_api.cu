@@ -5,6 +5,7 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -69,13 +70,30 @@ int n_params_expected(int problem, int dim) {
     return -1;
 }
 
+// mu~, nu~, c~ into the constant bank of the current device, once per device.
+std::mutex g_const_mu;
+bool g_const_done[64] = {};
+
+int upload_constants(irk_ctx *c) {
+    int dev = 0;
+    int rc = cuda_check(c, cudaGetDevice(&dev), "cudaGetDevice");
+    if (rc) return rc;
+    std::lock_guard<std::mutex> lk(g_const_mu);
+    if (dev < 64 && g_const_done[dev]) return IRK_OK;
+    if ((rc = cuda_check(c, cudaMemcpyToSymbol(irk::c_mu, c->T.mu, sizeof c->T.mu), "upload mu"))) return rc;
+    if ((rc = cuda_check(c, cudaMemcpyToSymbol(irk::c_nu, c->T.nu, sizeof c->T.nu), "upload nu"))) return rc;
+    if ((rc = cuda_check(c, cudaMemcpyToSymbol(irk::c_c, c->T.c, sizeof c->T.c), "upload c"))) return rc;
+    if (dev < 64) g_const_done[dev] = true;
+    return IRK_OK;
+}
+
 __global__ void advance_n_kernel(int64_t *n_done, int64_t nsteps) { *n_done += nsteps; }
 
 template <class P>
 int launch_g1(irk_ctx *c, const P &prob, double *y, double t0, char *ws, double *energy,
               int64_t *iters, cudaStream_t st) {
     EnsArgs a;
-    a.T = c->T;
+    for (int j = 0; j < 8; ++j) a.hb[j] = c->T.hb[j];
     a.y = y;
     a.n_done = reinterpret_cast<const int64_t *>(ws);
     a.hist = reinterpret_cast<double *>(ws + kHeader);
@@ -197,7 +215,8 @@ int irk_integrate(irk_ctx *c, double *y, double t0, void *workspace, double *ene
     if (c->energy_every > 0 && !energy) return fail(c, IRK_E_ARG, "irk_integrate: ENERGY_EVERY set but energy == NULL");
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
     char *ws = static_cast<char *>(workspace);
-    int rc;
+    int rc = upload_constants(c);
+    if (rc) return rc;
     switch (c->problem) {
     case IRK_KEPLER: {
         irk::Kepler P{c->params[0]};

@@ -4,6 +4,7 @@
 #include <cstdint>
 
 #include "../../include/irk_probe.h"
+#include "fp64.cuh"
 
 namespace {
 __global__ void __launch_bounds__(256) dfma_probe_kernel(double *out, int iters) {
@@ -28,4 +29,25 @@ extern "C" int64_t irk_probe_dfma(double *out, int blocks, int iters, void *stre
     dfma_probe_kernel<<<blocks, 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(out, iters);
     if (cudaGetLastError() != cudaSuccess) return -1;
     return (int64_t)blocks * 256 * iters * 16 * 2;
+}
+
+namespace {
+__global__ void divsqrt_probe_kernel(const double *a, const double *b, double *out, int64_t n) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    bool ok_d = true, ok_s = true;
+    const double qf = irk::ddiv_fast(a[i], b[i], ok_d);
+    const double sf = irk::dsqrt_fast(b[i], ok_s);
+    out[4 * i + 0] = ok_d ? qf : irk::ddiv(a[i], b[i]);
+    out[4 * i + 1] = irk::ddiv(a[i], b[i]);
+    out[4 * i + 2] = ok_s ? sf : irk::dsqrt(b[i]);
+    out[4 * i + 3] = irk::dsqrt(b[i]);
+}
+}  // namespace
+
+extern "C" int irk_probe_divsqrt(const double *a, const double *b, double *out, int64_t n, void *stream) {
+    if (!a || !b || !out || n < 0) return -1;
+    if (n == 0) return 0;
+    divsqrt_probe_kernel<<<(unsigned)((n + 255) / 256), 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(a, b, out, n);
+    return cudaGetLastError() == cudaSuccess ? 0 : -1;
 }

@@ -10,10 +10,13 @@ namespace irk {
 struct Kepler {
     static constexpr int d = 2;
     double GM;
-    __device__ __forceinline__ void accel(const double *q, double *a, double /*t*/) const {
+    // EXACT = false: branch-free fast paths, `ok` cleared if any needs the exact
+    // intrinsic (the caller then re-evaluates with EXACT = true); same bits.
+    template <bool EXACT>
+    __device__ __forceinline__ void accel(const double *q, double *a, double /*t*/, bool &ok) const {
         double r2 = dfma(q[0], q[0], dmul(q[1], q[1]));
-        double r3 = dmul(r2, dsqrt(r2));
-        double w = ddiv(GM, r3);
+        double r3 = dmul(r2, EXACT ? dsqrt(r2) : dsqrt_fast(r2, ok));
+        double w = EXACT ? ddiv(GM, r3) : ddiv_fast(GM, r3, ok);
         a[0] = -dmul(w, q[0]);
         a[1] = -dmul(w, q[1]);
     }
@@ -31,7 +34,8 @@ struct Kepler {
 struct HenonHeiles {
     static constexpr int d = 2;
     double lambda, xi;
-    __device__ __forceinline__ void accel(const double *q, double *a, double t) const {
+    template <bool EXACT>
+    __device__ __forceinline__ void accel(const double *q, double *a, double t, bool & /*ok*/) const {
         double aux = lambda;
         if (xi != 0.0) aux = dadd(lambda, dmul(xi, sin(t)));  // not bitwise vs libm
         a[0] = dsub(-q[0], dmul(dmul(dmul(2.0, aux), q[0]), q[1]));

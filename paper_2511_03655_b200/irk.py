@@ -22,7 +22,8 @@ LIB_PATH = os.path.join(_HERE, "lib", "libirk.so")
 
 SYMBOLS = ["irk_create", "irk_set_params", "irk_set_option", "irk_workspace_bytes",
            "irk_integrate", "irk_integrate_host", "irk_energy", "irk_stats", "irk_tableau",
-           "irk_set_comm", "irk_last_error", "irk_destroy", "irk_probe_dfma"]
+           "irk_set_comm", "irk_last_error", "irk_destroy", "irk_probe_dfma",
+           "irk_probe_divsqrt"]
 
 _lib = None
 _lock = threading.Lock()
@@ -61,6 +62,7 @@ def lib():
             l.irk_destroy.argtypes = [vp]
             l.irk_probe_dfma.argtypes = [vp, ctypes.c_int, ctypes.c_int, vp]
             l.irk_probe_dfma.restype = ctypes.c_int64
+            l.irk_probe_divsqrt.argtypes = [vp, vp, vp, ctypes.c_int64, vp]
             _lib = l
     return _lib
 
@@ -166,8 +168,10 @@ class Integrator:
         import torch
         out = np.zeros(4, dtype=np.int64)
         s = torch.cuda.current_stream(workspace.device) if stream is None else stream
-        rc = self._check(lib().irk_stats(self._ctx, _ptr(workspace), ctypes.c_void_p(s.cuda_stream),
-                                         out.ctypes.data_as(ctypes.POINTER(ctypes.c_int64))))
+        rc = lib().irk_stats(self._ctx, _ptr(workspace), ctypes.c_void_p(s.cuda_stream),
+                             out.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)))
+        if rc < 0 and rc != E_DIVERGED:  # E_DIVERGED is a device outcome, not a call error
+            self._check(rc)
         return rc, dict(maxiter_traj=int(out[0]), diverged_traj=int(out[1]),
                         first_bad_step=int(out[2]), total_sweeps=int(out[3]))
 
@@ -184,3 +188,14 @@ def probe_dfma(out, blocks: int, iters: int, stream) -> int:
     if n < 0:
         raise IrkError(E_CUDA, "irk_probe_dfma launch failed")
     return int(n)
+
+
+def probe_divsqrt(a, b, stream=None):
+    """(fast a/b, __ddiv_rn, fast sqrt b, __dsqrt_rn) for device float64 tensors a, b."""
+    import torch
+    n = a.numel()
+    out = torch.empty((n, 4), dtype=torch.float64, device=a.device)
+    s = torch.cuda.current_stream(a.device) if stream is None else stream
+    if lib().irk_probe_divsqrt(_ptr(a), _ptr(b), _ptr(out), n, ctypes.c_void_p(s.cuda_stream)):
+        raise IrkError(E_CUDA, "irk_probe_divsqrt failed")
+    return out

@@ -1,0 +1,30 @@
+"""Run one irk_integrate of a config (for ncu / compute-sanitizer captures)."""
+import argparse
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+import torch  # noqa: E402
+
+from paper_2511_03655_b200 import irk, workloads as wl  # noqa: E402
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--config", type=int, default=2)
+ap.add_argument("--batch", type=int, default=0)
+ap.add_argument("--nsteps", type=int, default=0)
+ap.add_argument("--reps", type=int, default=1)
+a = ap.parse_args()
+kw = {}
+if a.batch:
+    kw["batch"] = a.batch
+if a.nsteps:
+    kw["nsteps"] = a.nsteps
+w = wl.config(a.config, **kw)
+with irk.Integrator(w.problem, w.dim, w.h, w.nsteps, w.batch, w.params) as ig:
+    y = torch.tensor(w.y, dtype=torch.float64, device="cuda")
+    for _ in range(a.reps):
+        ws = ig.new_workspace()
+        ig.integrate(y, ws)
+    torch.cuda.synchronize()
+    print("rc", ig.stats(ws))
