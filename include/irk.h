@@ -62,7 +62,10 @@ enum irk_option {
     IRK_OPT_MODE = 1,         /* 0 = partitioned (default, Eq. IRK_FP2), 1 = first-order (Eq. IRK_FP) */
     IRK_OPT_MAX_ITERS = 2,    /* sweeps cap per step, default 100 (flagged, step accepted)   */
     IRK_OPT_ENERGY_EVERY = 3, /* E > 0: sample H(y_n) at local steps 0, E, 2E, ... (default 0) */
-    IRK_OPT_MAPPING = 4       /* 0 = auto; see DESIGN.md for the per-problem kernels          */
+    IRK_OPT_MAPPING = 4,      /* 0 = auto; see DESIGN.md for the per-problem kernels          */
+    IRK_OPT_BALANCE = 5       /* ensemble scheduling: -1 = auto (default), 0 = off, C > 0 = run the
+                                 call in chunks of C steps, re-sorting trajectories by the cost of
+                                 the previous chunk (bitwise-neutral)  */
 };
 
 /* Create a context for `batch` independent trajectories of `problem` in
@@ -81,7 +84,8 @@ int irk_set_option(irk_ctx *ctx, int key, int64_t val);
 /* Bytes of caller-owned DEVICE workspace irk_integrate needs.  Layout: a
  * 64-byte header {int64 n_done, ...}, then the history L_{n-1} [8][dim][batch]
  * fp64, then per-trajectory stats [4][batch] int64 {maxiter_hits, diverged_step
- * (1-based absolute step, 0 = none), sweeps_total, reserved}.  A zero-filled workspace means "first
+ * (1-based absolute step, 0 = none), sweeps_total, reserved}, then scheduler scratch
+ * (int32 permutation and cost-sort buffers).  A zero-filled workspace means "first
  * step" (zero history, n_done = 0); reusing it continues the integration bitwise
  * as if uninterrupted (t_{n-1} = t0 + (n-1) h with the absolute n). */
 size_t irk_workspace_bytes(const irk_ctx *ctx);

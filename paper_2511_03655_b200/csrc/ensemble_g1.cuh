@@ -39,8 +39,12 @@ struct EnsArgs {
     int64_t *stats;       // [4][batch]
     const int64_t *n_done;
     double *energy;       // [(nsteps/E)+1][batch] or null
-    int64_t *iters;       // [batch] or null
+    int64_t *iters;       // [batch] or null (set on the first chunk, accumulated after)
+    const int32_t *perm;  // thread slot -> trajectory (null = identity; < 0 = idle slot)
+    int32_t *csweeps;     // [batch] sweeps of this chunk, for the cost sort (or null)
     int64_t batch, nsteps, energy_every;
+    int64_t c0;           // call-local index of this chunk's first step
+    int64_t nslots;       // launched thread slots (perm covers all of them)
     double h, t0;
     int max_iters;
 };
@@ -52,11 +56,13 @@ __global__ void __launch_bounds__(G1_THREADS, 8) ens_g1_kernel(const __grid_cons
                                                     const __grid_constant__ P prob) {
     constexpr int d = P::d, D = 2 * d;
     const int64_t B = a.batch;
-    const int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    const int64_t slot = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     __shared__ __align__(16) double sW[2][64];  // [0] = mu~, [1] = nu~ (row-major)
     for (int e = threadIdx.x; e < 128; e += blockDim.x) sW[e >> 6][e & 63] = (e < 64) ? (&c_mu[0][0])[e] : (&c_nu[0][0])[e - 64];
     __syncthreads();
-    if (b >= B) return;
+    if (slot >= a.nslots) return;
+    const int64_t b = a.perm ? (int64_t)a.perm[slot] : slot;
+    if (b < 0 || b >= B) return;
 
     int64_t bad = a.stats[1 * B + b];
     int64_t hits = 0, sweeps = 0;
@@ -74,9 +80,10 @@ __global__ void __launch_bounds__(G1_THREADS, 8) ens_g1_kernel(const __grid_cons
     }
     const int64_t n0 = *a.n_done;
     const bool sample = (a.energy != nullptr) && (a.energy_every > 0);
-    if (sample) a.energy[b] = prob.energy(q, v);
+    if (sample && a.c0 == 0) a.energy[b] = prob.energy(q, v);
     if (bad > 0 || a.nsteps == 0) {  // frozen (diverged at step `bad`, 1-based) or nothing to do
-        if (a.iters) a.iters[b] = 0;
+        if (a.iters && a.c0 == 0) a.iters[b] = 0;
+        if (a.csweeps) a.csweeps[b] = 0;
         return;
     }
     {   // a1: nu-init from the history (zeros = first step)
@@ -207,8 +214,8 @@ __global__ void __launch_bounds__(G1_THREADS, 8) ens_g1_kernel(const __grid_cons
             k = 0;
 #pragma unroll
             for (int l = 0; l < d; ++l) sM[l][tx] = sP[l][tx] = kInf;
-            if (sample && (n % a.energy_every) == 0)
-                a.energy[(n / a.energy_every) * B + b] = prob.energy(q, v);
+            if (sample && ((a.c0 + n) % a.energy_every) == 0)
+                a.energy[((a.c0 + n) / a.energy_every) * B + b] = prob.energy(q, v);
             if (n == a.nsteps || !finite) {  // history = Lv (Eq. IRK_init2 extrapolates only
                                              // velocities); the q block is zeroed (R-4)
 #pragma unroll
@@ -255,7 +262,8 @@ __global__ void __launch_bounds__(G1_THREADS, 8) ens_g1_kernel(const __grid_cons
     a.stats[0 * B + b] += hits;
     a.stats[1 * B + b] = bad;
     a.stats[2 * B + b] += sweeps;
-    if (a.iters) a.iters[b] = sweeps;
+    if (a.iters) a.iters[b] = (a.c0 == 0) ? sweeps : a.iters[b] + sweeps;
+    if (a.csweeps) a.csweeps[b] = (int32_t)sweeps;
 }
 
 }  // namespace irk

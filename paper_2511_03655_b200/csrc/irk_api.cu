@@ -10,6 +10,7 @@
 #include <vector>
 
 #include "../../include/irk.h"
+#include "balance.cuh"
 #include "ensemble_g1.cuh"
 #include "problems.cuh"
 #include "tableau.h"
@@ -26,6 +27,7 @@ struct irk_ctx {
     std::vector<double> params;
     bool have_params = false;
     int mode = 0, max_iters = 100, mapping = 0;
+    int64_t balance = -1;  // IRK_OPT_BALANCE: -1 auto, 0 off, >0 chunk length
     int64_t energy_every = 0;
     Tableau T;
     std::string err;
@@ -89,6 +91,32 @@ int upload_constants(irk_ctx *c) {
 
 __global__ void advance_n_kernel(int64_t *n_done, int64_t nsteps) { *n_done += nsteps; }
 
+// Workspace regions after the stats block (irk_workspace_bytes).
+struct Sched {
+    int32_t *perm, *csweeps, *sorted, *bins;
+};
+int64_t g1_slots(int64_t B) { return (B + irk::G1_THREADS - 1) / irk::G1_THREADS * irk::G1_THREADS; }
+size_t sched_bytes(const irk_ctx *c) {
+    return sizeof(int32_t) * ((size_t)g1_slots(c->batch) + 2 * (size_t)c->batch + irk::kCostBins);
+}
+Sched sched_of(const irk_ctx *c, char *ws) {
+    Sched s;
+    s.perm = reinterpret_cast<int32_t *>(ws + kHeader + hist_bytes(c) + stats_bytes(c));
+    s.csweeps = s.perm + g1_slots(c->batch);
+    s.sorted = s.csweeps + c->batch;
+    s.bins = s.sorted + c->batch;
+    return s;
+}
+
+// chunk length of the cost-balanced schedule (0 = one launch, identity order)
+int64_t balance_chunk(const irk_ctx *c) {
+    if (c->balance == 0 || c->nsteps == 0) return 0;
+    if (c->balance > 0) return c->balance < c->nsteps ? c->balance : 0;
+    if (c->batch < 8192) return 0;  // auto: only worth it with many warps per SM
+    int64_t ch = (c->nsteps + 7) / 8;
+    return ch < c->nsteps ? ch : 0;
+}
+
 template <class P>
 int launch_g1(irk_ctx *c, const P &prob, double *y, double t0, char *ws, double *energy,
               int64_t *iters, cudaStream_t st) {
@@ -101,15 +129,53 @@ int launch_g1(irk_ctx *c, const P &prob, double *y, double t0, char *ws, double 
     a.energy = energy;
     a.iters = iters;
     a.batch = c->batch;
-    a.nsteps = c->nsteps;
     a.energy_every = c->energy_every;
     a.h = c->h;
     a.t0 = t0;
     a.max_iters = c->max_iters;
-    const int threads = 64;
+    const int threads = irk::G1_THREADS;
     const int64_t blocks = (c->batch + threads - 1) / threads;
-    irk::ens_g1_kernel<P><<<(unsigned)blocks, threads, 0, st>>>(a, prob);
-    return cuda_check(c, cudaGetLastError(), "ens_g1_kernel launch");
+    const int64_t chunk = balance_chunk(c);
+    if (chunk == 0) {  // single launch over all steps, identity assignment
+        a.nsteps = c->nsteps;
+        a.c0 = 0;
+        a.perm = nullptr;
+        a.csweeps = nullptr;
+        a.nslots = c->batch;
+        irk::ens_g1_kernel<P><<<(unsigned)blocks, threads, 0, st>>>(a, prob);
+        int rc = cuda_check(c, cudaGetLastError(), "ens_g1_kernel launch");
+        if (rc) return rc;
+        advance_n_kernel<<<1, 1, 0, st>>>(reinterpret_cast<int64_t *>(ws), c->nsteps);
+        return cuda_check(c, cudaGetLastError(), "advance_n launch");
+    }
+    Sched sc = sched_of(c, ws);
+    for (int64_t c0 = 0; c0 < c->nsteps; c0 += chunk) {
+        const int64_t steps = (c->nsteps - c0 < chunk) ? c->nsteps - c0 : chunk;
+        a.nsteps = steps;
+        a.c0 = c0;
+        a.csweeps = sc.csweeps;
+        if (c0 == 0) {
+            a.perm = nullptr;
+            a.nslots = c->batch;
+        } else {  // sort by the previous chunk's sweeps, deal warps to blocks
+            const unsigned sb = (unsigned)((c->batch + 255) / 256 < 1184 ? (c->batch + 255) / 256 : 1184);
+            cudaMemsetAsync(sc.bins, 0, sizeof(int32_t) * irk::kCostBins, st);
+            irk::cost_hist_kernel<<<sb, 256, 0, st>>>(sc.csweeps, c->batch, chunk, sc.bins);
+            irk::cost_scan_kernel<<<1, irk::kCostBins, 0, st>>>(sc.bins);
+            irk::cost_scatter_kernel<<<sb, 256, 0, st>>>(sc.csweeps, c->batch, chunk, sc.bins, sc.sorted);
+            const int64_t nslots = g1_slots(c->batch);
+            irk::cost_perm_kernel<<<(unsigned)((nslots + 255) / 256), 256, 0, st>>>(sc.sorted, c->batch, blocks,
+                                                                                      threads, sc.perm);
+            a.perm = sc.perm;
+            a.nslots = nslots;
+        }
+        irk::ens_g1_kernel<P><<<(unsigned)blocks, threads, 0, st>>>(a, prob);
+        int rc = cuda_check(c, cudaGetLastError(), "ens_g1_kernel launch");
+        if (rc) return rc;
+        advance_n_kernel<<<1, 1, 0, st>>>(reinterpret_cast<int64_t *>(ws), steps);
+        if ((rc = cuda_check(c, cudaGetLastError(), "advance_n launch"))) return rc;
+    }
+    return IRK_OK;
 }
 
 template <class P>
@@ -193,6 +259,10 @@ int irk_set_option(irk_ctx *c, int key, int64_t val) {
         if (val < 0) return fail(c, IRK_E_ARG, "irk_set_option: ENERGY_EVERY < 0");
         c->energy_every = val;
         return IRK_OK;
+    case IRK_OPT_BALANCE:
+        if (val < -1) return fail(c, IRK_E_ARG, "irk_set_option: bad BALANCE");
+        c->balance = val;
+        return IRK_OK;
     case IRK_OPT_MAPPING:
         if (val < 0) return fail(c, IRK_E_ARG, "irk_set_option: bad MAPPING");
         c->mapping = (int)val;
@@ -203,7 +273,7 @@ int irk_set_option(irk_ctx *c, int key, int64_t val) {
 
 size_t irk_workspace_bytes(const irk_ctx *c) {
     if (!c) return 0;
-    return kHeader + hist_bytes(c) + stats_bytes(c);
+    return kHeader + hist_bytes(c) + stats_bytes(c) + sched_bytes(c);
 }
 
 int irk_integrate(irk_ctx *c, double *y, double t0, void *workspace, double *energy, int64_t *iters,
@@ -230,9 +300,7 @@ int irk_integrate(irk_ctx *c, double *y, double t0, void *workspace, double *ene
     }
     default: return fail(c, IRK_E_ARG, "irk_integrate: problem not supported");
     }
-    if (rc) return rc;
-    advance_n_kernel<<<1, 1, 0, st>>>(reinterpret_cast<int64_t *>(ws), c->nsteps);
-    return cuda_check(c, cudaGetLastError(), "advance_n launch");
+    return rc;
 }
 
 int irk_integrate_host(irk_ctx *c, double *y_host, double t0, double *energy_host, int64_t *iters_host,

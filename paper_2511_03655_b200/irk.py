@@ -14,7 +14,7 @@ import numpy as np
 
 KEPLER, NBODY, FPU_BETA, HENON_HEILES, NBODY_DIRECT = 1, 2, 3, 4, 5
 OK, W_MAXITER, E_ARG, E_CUDA, E_DIVERGED, E_COMM, E_STATE = 0, 1, -1, -2, -3, -4, -5
-OPT_MODE, OPT_MAX_ITERS, OPT_ENERGY_EVERY, OPT_MAPPING = 1, 2, 3, 4
+OPT_MODE, OPT_MAX_ITERS, OPT_ENERGY_EVERY, OPT_MAPPING, OPT_BALANCE = 1, 2, 3, 4, 5
 PARTITIONED, FIRST_ORDER = 0, 1
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
@@ -89,7 +89,7 @@ class Integrator:
 
     def __init__(self, problem: int, dim: int, h: float, nsteps: int, batch: int, params,
                  *, mode: int = PARTITIONED, max_iters: int = 100, energy_every: int = 0,
-                 mapping: int = 0):
+                 mapping: int = 0, balance: int = -1):
         L = lib()
         self._ctx = L.irk_create(problem, dim, h, nsteps, batch)
         if not self._ctx:
@@ -99,7 +99,8 @@ class Integrator:
         p = np.ascontiguousarray(params, dtype=np.float64)
         self._check(L.irk_set_params(self._ctx, _dp(p), len(p)))
         for key, val in ((OPT_MODE, mode), (OPT_MAX_ITERS, max_iters),
-                         (OPT_ENERGY_EVERY, energy_every), (OPT_MAPPING, mapping)):
+                         (OPT_ENERGY_EVERY, energy_every), (OPT_MAPPING, mapping),
+                         (OPT_BALANCE, balance)):
             self._check(L.irk_set_option(self._ctx, key, val))
 
     def _check(self, rc):

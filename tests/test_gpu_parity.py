@@ -207,3 +207,29 @@ def test_fast_div_sqrt_bitwise(irk):
     out = irk.probe_divsqrt(A, B).cpu().numpy()
     np.testing.assert_array_equal(out[:, 0].view(np.int64), out[:, 1].view(np.int64))
     np.testing.assert_array_equal(out[:, 2].view(np.int64), out[:, 3].view(np.int64))
+
+
+def test_cost_balanced_schedule_is_bitwise_neutral(irk, orc):
+    """Chunked, cost-sorted scheduling (IRK_OPT_BALANCE) only changes which
+    thread runs which trajectory: results equal the single-launch run and the
+    oracle bit for bit, including energy samples that straddle chunks."""
+    w = wl.kepler_ensemble(batch=9000, nsteps=1000)
+    outs = []
+    for bal in (0, 230, -1):
+        with irk.Integrator(w.problem, w.dim, w.h, w.nsteps, w.batch, w.params, energy_every=100,
+                            balance=bal) as ig:
+            Y = torch.tensor(w.y, dtype=torch.float64, device="cuda")
+            ws = ig.new_workspace()
+            E = torch.zeros((ig.n_energy(), w.batch), dtype=torch.float64, device="cuda")
+            it = torch.zeros(w.batch, dtype=torch.int64, device="cuda")
+            ig.integrate(Y, ws, energy=E, iters=it)
+            rc, st = ig.stats(ws)
+            outs.append((Y.cpu().numpy(), E.cpu().numpy(), it.cpu().numpy(), st["total_sweeps"]))
+    for o in outs[1:]:
+        assert np.array_equal(o[0], outs[0][0]) and np.array_equal(o[1], outs[0][1])
+        assert np.array_equal(o[2], outs[0][2]) and o[3] == outs[0][3]
+    idx = np.arange(0, w.batch, 97)
+    orr = orc.integrate(w.problem, w.y[:, idx], w.params, w.h, w.nsteps, energy_every=100)
+    assert np.array_equal(outs[1][0][:, idx], orr["y"])
+    assert np.array_equal(outs[1][1][:, idx], orr["energy"])
+    assert np.array_equal(outs[1][2][idx], orr["iters"])

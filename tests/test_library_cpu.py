@@ -78,7 +78,7 @@ def test_params_and_options_errors(irk):
     with pytest.raises(irk.IrkError):
         irk.Integrator(irk.KEPLER, 4, 0.1, 10, 4, params=[1.0], max_iters=0)
     w = irk.Integrator(irk.KEPLER, 4, -0.1, 10, 4, params=[1.0])  # negative h is allowed
-    assert w.workspace_bytes == 64 + 8 * 8 * 4 * 4 + 8 * 4 * 4
+    assert w.workspace_bytes == 64 + 8 * 8 * 4 * 4 + 8 * 4 * 4 + 4 * (64 + 2 * 4 + 1024)
     w.close()
 
 
