@@ -144,7 +144,7 @@ def run_reference(args):
     import numpy as np
     w = wl.kepler_ensemble()
     cores = os.cpu_count() or 1
-    S = cores * 4
+    S = cores * 48  # ~1 s of oracle work per step on the GPU box's host
     ysub = np.ascontiguousarray(w.y[:, :S])
     for _ in range(args.warmup):
         oracle.integrate(w.problem, ysub, w.params, w.h, 500, nthreads=cores)
@@ -261,7 +261,7 @@ def run_ours(args):
         traffic = None
         tp = os.path.join(ROOT, "profiles", "traffic.json")
         if os.path.exists(tp):
-            traffic = json.load(open(tp)).get("config2_kepler_ensemble")
+            traffic = json.load(open(tp)).get("config2_kepler_ensemble")  # bytes per chunk launch
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": warm, "ms_per_step": 1e3 * T / args.steps, "higher_is_better": True,
@@ -274,6 +274,7 @@ def run_ours(args):
                        "parallelism": f"trajectory-sharded x{world}, no collective"},
             "roofline": {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                          "frac": achieved / peak, "traffic": traffic,
+                         "traffic_unit": "DRAM bytes per ens_g1 chunk launch (ncu --set full, profiles/r1)",
                          "peak_note": f"FP64 pipe: {SM_COUNT} SM x {FP64_FMA_PER_CLK_PER_SM} FMA/clk x 2 x {sm_max:.0f} MHz; "
                                       f"DFMA probe measured {probe:.2f} TFLOP/s on this GPU",
                          "kernel": "ens_g1_kernel<Kepler>", "flops_per_launch": fl,

@@ -44,8 +44,11 @@ def _stale() -> bool:
     return any(os.path.getmtime(p) > t for p in deps if os.path.exists(p))
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not _stale():
+def build(force: bool = False, verbose: bool = False, out: str | None = None,
+          defines: tuple = ()) -> str:
+    """Compile libirk.so (or, for A/B experiments, a variant with extra -D flags to `out`)."""
+    lib_path = out or LIB
+    if not force and out is None and not _stale():
         return LIB
     os.makedirs(OUT, exist_ok=True)
     bdir = os.path.join(OUT, "obj")
@@ -60,22 +63,23 @@ def build(force: bool = False, verbose: bool = False) -> str:
     log = []
     for src in CU_SOURCES:
         o = os.path.join(bdir, src + ".o")
-        r = subprocess.run([nvcc, *NVCC_FLAGS, "-I", os.path.join(ROOT, "include"), "-c",
+        r = subprocess.run([nvcc, *NVCC_FLAGS, *[f"-D{x}" for x in defines], "-I", os.path.join(ROOT, "include"), "-c",
                             os.path.join(CSRC, src), "-o", o], capture_output=True, text=True)
         log.append(r.stdout + r.stderr)
         if r.returncode:
             sys.stderr.write(r.stdout + r.stderr)
             raise RuntimeError(f"nvcc failed on {src}")
         objs.append(o)
-    tmp = LIB + f".tmp{os.getpid()}"
+    tmp = lib_path + f".tmp{os.getpid()}"
+    os.makedirs(os.path.dirname(lib_path), exist_ok=True)
     subprocess.check_call([nvcc, "-shared", *GENCODE, "-Xcompiler", "-fPIC", "-o", tmp, *objs,
                            "-cudart", "static"])
-    os.replace(tmp, LIB)
-    with open(os.path.join(OUT, "ptxas.log"), "w") as f:
+    os.replace(tmp, lib_path)
+    with open(lib_path + ".ptxas.log" if out else os.path.join(OUT, "ptxas.log"), "w") as f:
         f.write("\n".join(log))
     if verbose:
         print("\n".join(log))
-    return LIB
+    return lib_path
 
 
 if __name__ == "__main__":

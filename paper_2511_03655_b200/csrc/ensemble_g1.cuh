@@ -50,9 +50,15 @@ struct EnsArgs {
 };
 
 constexpr int G1_THREADS = 64;
+#ifndef G1_MAXREG
+#define G1_MAXREG 168    // measured best on config 2 (tools/variants.py): 128: 116 ms, 144: 136, 168: 107, 190+: 109-111
+#endif
+#ifndef G1_RHS_ILP
+#define G1_RHS_ILP 8     // stages per trip of the RHS loop (8: 107 ms, 4: 145 ms at 168 regs)
+#endif
 
 template <class P>
-__global__ void __launch_bounds__(G1_THREADS, 8) ens_g1_kernel(const __grid_constant__ EnsArgs a,
+__global__ void __maxnreg__(G1_MAXREG) ens_g1_kernel(const __grid_constant__ EnsArgs a,
                                                     const __grid_constant__ P prob) {
     constexpr int d = P::d, D = 2 * d;
     const int64_t B = a.batch;
@@ -162,15 +168,15 @@ __global__ void __launch_bounds__(G1_THREADS, 8) ens_g1_kernel(const __grid_cons
                 stop = stop && ok;
             }
         }
-        // a3 + a4 (first half): F_i = g(Q_i, t_i) ; Lv_i = hb_i F_i, two stages per trip
-        // (enough ILP for the branch-free div/sqrt chains without spilling).
+        // a3 + a4 (first half): F_i = g(Q_i, t_i) ; Lv_i = hb_i F_i, G1_RHS_ILP stages per
+        // trip (ILP for the ~20-deep dependent div/sqrt chains, bounded register use).
         const double tn1 = dadd(a.t0, dmul((double)(n0 + n), a.h));
         {
             bool ok = true;
 #pragma unroll 1
-            for (int i0 = 0; i0 < 8; i0 += 2) {
+            for (int i0 = 0; i0 < 8; i0 += G1_RHS_ILP) {
 #pragma unroll
-                for (int i = i0; i < i0 + 2; ++i) {
+                for (int i = i0; i < i0 + G1_RHS_ILP; ++i) {
                     double Qi[d], Fi[d];
 #pragma unroll
                     for (int l = 0; l < d; ++l) Qi[l] = sQ[i * d + l][tx];

@@ -18,7 +18,7 @@ OPT_MODE, OPT_MAX_ITERS, OPT_ENERGY_EVERY, OPT_MAPPING, OPT_BALANCE = 1, 2, 3, 4
 PARTITIONED, FIRST_ORDER = 0, 1
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "lib", "libirk.so")
+LIB_PATH = os.environ.get("IRK_LIB_OVERRIDE") or os.path.join(_HERE, "lib", "libirk.so")  # override: A/B builds only
 
 SYMBOLS = ["irk_create", "irk_set_params", "irk_set_option", "irk_workspace_bytes",
            "irk_integrate", "irk_integrate_host", "irk_energy", "irk_stats", "irk_tableau",

@@ -1,0 +1,51 @@
+"""A/B timing of library build variants (-D flags) on config 2 (one call each)."""
+import json
+import os
+import subprocess
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+VARIANTS = json.loads(os.environ.get("IRK_VARIANTS", "{}"))
+
+
+def build_all():
+    from paper_2511_03655_b200 import build
+    for name, defs in VARIANTS.items():
+        out = os.path.join(ROOT, "paper_2511_03655_b200", "lib", "variants", f"libirk_{name}.so")
+        build.build(force=True, out=out, defines=tuple(defs))
+        log = open(out + ".ptxas.log").read()
+        import re
+        m = re.findall(r"ens_g1_kernelINS_6Kepler.*?\n(.*?)\n(.*?)\n", log, re.S)
+        print(name, m[0] if m else "")
+
+
+def time_one(name):
+    lib = os.path.join(ROOT, "paper_2511_03655_b200", "lib", "variants", f"libirk_{name}.so")
+    code = f"""
+import os, sys, torch
+os.environ['IRK_LIB_OVERRIDE'] = {lib!r}
+sys.path.insert(0, {ROOT!r})
+from paper_2511_03655_b200 import irk, workloads as wl
+w = wl.kepler_ensemble()
+ig = irk.Integrator(w.problem, w.dim, w.h, w.nsteps, w.batch, w.params)
+y0 = torch.tensor(w.y, device='cuda'); Y = torch.empty_like(y0); ws = ig.new_workspace()
+ts = []
+for r in range(4):
+    Y.copy_(y0); ws.zero_(); torch.cuda.synchronize()
+    e0 = torch.cuda.Event(enable_timing=True); e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(); ig.integrate(Y, ws); e1.record(); torch.cuda.synchronize()
+    ts.append(e0.elapsed_time(e1))
+print({name!r}, 'ms', min(ts[1:]), ts)
+"""
+    r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True)
+    print(r.stdout.strip() or r.stderr[-500:])
+
+
+if __name__ == "__main__":
+    if sys.argv[1] == "build":
+        build_all()
+    else:
+        for n in VARIANTS:
+            time_one(n)
