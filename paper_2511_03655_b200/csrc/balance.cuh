@@ -56,20 +56,21 @@ __global__ void cost_scatter_kernel(const int32_t *csweeps, int64_t B, int64_t s
     }
 }
 
-// slot -> trajectory: warp W of the sorted order holds ranks [32W, 32W+32);
-// block b (threads_per_block = 64) runs warps b and 2*nblocks-1-b.
-__global__ void cost_perm_kernel(const int32_t *sorted, int64_t B, int64_t nblocks, int threads_per_block,
+// slot -> trajectory.  A kernel warp holds `spw` trajectory slots (32 for ens_g1,
+// 32/NB groups for ens_nbody) and a block holds `wpb` warps.  Warp W of the
+// sorted order holds ranks [spw*W, spw*W + spw); block blk runs warps blk*wpb/2..
+// from the front of the order and as many from the back (mirrored dealing).
+__global__ void cost_perm_kernel(const int32_t *sorted, int64_t B, int64_t nblocks, int wpb, int spw,
                                  int32_t *perm) {
     const int64_t slot = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (slot >= nblocks * threads_per_block) return;
-    const int64_t blk = slot / threads_per_block;
-    const int wib = (int)((slot % threads_per_block) / 32), lane = (int)(slot % 32);
-    const int wpb = threads_per_block / 32;
-    // warps of block blk: alternate from the front and from the back of the order
+    const int64_t per_block = (int64_t)wpb * spw;
+    if (slot >= nblocks * per_block) return;
+    const int64_t blk = slot / per_block;
+    const int wib = (int)((slot % per_block) / spw), s = (int)(slot % spw);
     const int64_t nw = nblocks * wpb;
-    const int64_t k = blk * wpb + wib;  // 0..nw-1
-    const int64_t W = (wib % 2 == 0) ? (k / 2) : (nw - 1 - k / 2);
-    const int64_t rank = W * 32 + lane;
+    const int64_t kk = blk * wpb + wib;  // 0..nw-1
+    const int64_t W = (wib % 2 == 0) ? (kk / 2) : (nw - 1 - kk / 2);
+    const int64_t rank = W * spw + s;
     perm[slot] = (rank < B) ? sorted[rank] : -1;
 }
 

@@ -1,0 +1,34 @@
+// Shared declarations of the ensemble kernels: coefficient constants and the
+// launch-argument block.
+#pragma once
+#include <cstdint>
+
+#include "tableau.h"
+
+namespace irk {
+
+// mu~, nu~ and c~ do not depend on h: one copy per device in the constant bank
+// (uploaded once per device by irk_api.cu), read as uniform operands.  hb~ =
+// fl(h b~) depends on h and travels in the kernel parameters.
+__constant__ double c_mu[8][8];
+__constant__ double c_nu[8][8];
+__constant__ double c_c[8];
+
+struct EnsArgs {
+    double hb[8];
+    double *y;            // [dim][batch]
+    double *hist;         // [8][dim][batch]
+    int64_t *stats;       // [4][batch]
+    const int64_t *n_done;
+    double *energy;       // [(nsteps/E)+1][batch] or null
+    int64_t *iters;       // [batch] or null (set on the first chunk, accumulated after)
+    const int32_t *perm;  // thread slot -> trajectory (null = identity; < 0 = idle slot)
+    int32_t *csweeps;     // [batch] sweeps of this chunk, for the cost sort (or null)
+    int64_t batch, nsteps, energy_every;
+    int64_t c0;           // call-local index of this chunk's first step
+    int64_t nslots;       // launched thread slots (perm covers all of them)
+    double h, t0;
+    int max_iters;
+};
+
+}  // namespace irk

@@ -1,0 +1,352 @@
+// Ensemble kernel, mapping "body-per-lane": one group of NB lanes per
+// trajectory of a small gravitational N-body system (config 3: NB = 6, d = 18);
+// lane k of a group owns body k -- its 3 position and 3 velocity components for
+// all 8 stages.  32/NB groups share a warp (5 for NB = 6).
+//
+// Why this mapping: a 6-body stage tile is 3 x 144
+// doubles, too large for one thread's registers or for one thread per
+// trajectory in shared memory at 111 trajectories per SM; splitting by body makes
+// both 8x8 contractions (a1, a2, a4) thread-local (components are independent)
+// and leaves only the RHS (a3) needing other bodies' stage positions, which the
+// group exchanges through a shared-memory tile that doubles as Q^[k-1] for the
+// stop test.
+//
+// Canonical RHS (R-8, oracle accel_nbody_pairs): body k accumulates
+// its acceleration over the pairs that contain it in lexicographic pair order,
+// i.e. over j = 0..NB-1, j != k ascending, with d = q_k - q_j and
+// s = -(m_j w) for j < k, d = q_j - q_k and s = m_j w for j > k,
+// w = G / (r2 sqrt(r2)), r2 = fma(dz,dz,fma(dy,dy,fma(dx,dx,eps^2))),
+// a_k = fma(s, d, a_k).  Both lanes of a pair evaluate w with identical
+// operations, so the sum is bitwise the oracle's.
+//
+// The loop is warp-uniform (it runs until every group of the warp is done;
+// finished groups idle) so that __syncwarp / __ballot_sync always see the full
+// warp.  Sweep-granular as in ens_g1: a group whose step converged updates and
+// re-initialises in the same trip.
+#pragma once
+#include <cstdint>
+
+#include "ens_common.cuh"
+#include "fp64.cuh"
+
+namespace irk {
+
+struct NBodyParams {
+    double G, eps2;
+    double m[16];
+};
+
+constexpr int NB_THREADS = 64;
+
+// Hamiltonian of one system from shared memory (canonical term order, Neumaier;
+// oracle energy_nbody): kinetic terms i = 0..N-1, then row sums over j > i.
+template <int NB>
+__device__ double nbody_energy(const double *qv, const NBodyParams &P) {
+    const double *q = qv, *v = qv + 3 * NB;
+    Neumaier tot;
+    for (int i = 0; i < NB; ++i) {
+        double k = dfma(v[3 * i + 2], v[3 * i + 2], dfma(v[3 * i + 1], v[3 * i + 1], dmul(v[3 * i], v[3 * i])));
+        tot.add(dmul(dmul(0.5, P.m[i]), k));
+    }
+    for (int i = 0; i < NB; ++i) {
+        Neumaier row;
+        for (int j = i + 1; j < NB; ++j) {
+            double dx = dsub(q[3 * j], q[3 * i]);
+            double dy = dsub(q[3 * j + 1], q[3 * i + 1]);
+            double dz = dsub(q[3 * j + 2], q[3 * i + 2]);
+            double r2 = dfma(dz, dz, dfma(dy, dy, dfma(dx, dx, P.eps2)));
+            row.add(-ddiv(dmul(P.G, dmul(P.m[i], P.m[j])), dsqrt(r2)));
+        }
+        tot.add(row.result());
+    }
+    return tot.result();
+}
+
+template <int NB>
+__global__ void __launch_bounds__(NB_THREADS) ens_nbody_kernel(const __grid_constant__ EnsArgs a,
+                                                               const __grid_constant__ NBodyParams P) {
+    constexpr int GPW = 32 / NB;                 // groups (trajectories) per warp
+    constexpr int GPB = GPW * (NB_THREADS / 32);  // groups per block
+    constexpr int d = 3 * NB, D = 6 * NB;
+    const unsigned FULL = 0xffffffffu;
+    const int64_t B = a.batch;
+
+    __shared__ __align__(16) double sW[2][64];         // mu~, nu~ for the per-group choice in a4
+    __shared__ double sQ[GPB][8][d];                    // Q^[k] of every body and stage (+ Q^[k-1] for Delta)
+    __shared__ double sQV[GPB][D];                      // (q, v) gathered for energy samples
+    __shared__ double sm[NB];
+    for (int e = threadIdx.x; e < 128; e += blockDim.x)
+        sW[e >> 6][e & 63] = (e < 64) ? (&c_mu[0][0])[e] : (&c_nu[0][0])[e - 64];
+    for (int e = threadIdx.x; e < NB; e += blockDim.x) sm[e] = P.m[e];
+    __syncthreads();
+
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int grp = lane / NB, body = lane % NB;
+    const bool lane_ok = grp < GPW;
+    const int gib = warp * GPW + (lane_ok ? grp : 0);   // group index inside the block
+    const int64_t slot = (int64_t)blockIdx.x * GPB + gib;
+    int64_t b = -1;
+    if (lane_ok && slot < a.nslots) b = a.perm ? (int64_t)a.perm[slot] : slot;
+    if (b >= B) b = -1;
+    const bool valid = b >= 0;
+    const unsigned gmask = lane_ok ? (((1u << NB) - 1u) << (grp * NB)) : 0u;
+
+    double q[3] = {0, 0, 0}, v[3] = {0, 0, 0};
+    int64_t bad = 0;
+    if (valid) {
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            q[c] = a.y[(int64_t)(3 * body + c) * B + b];
+            v[c] = a.y[(int64_t)(d + 3 * body + c) * B + b];
+        }
+        bad = a.stats[1 * B + b];
+    }
+    const int64_t n0 = *a.n_done;
+    const bool sample = (a.energy != nullptr) && (a.energy_every > 0);
+    // energy at local step 0 (first chunk only)
+    if (sample && a.c0 == 0) {
+        if (lane_ok) {
+#pragma unroll
+            for (int c = 0; c < 3; ++c) {
+                sQV[gib][3 * body + c] = q[c];
+                sQV[gib][d + 3 * body + c] = v[c];
+            }
+        }
+        __syncwarp();
+        if (valid && body == 0) a.energy[b] = nbody_energy<NB>(sQV[gib], P);
+        __syncwarp();
+    }
+    bool live = valid && bad == 0 && a.nsteps > 0;
+    if (valid && !live) {
+        if (a.iters && a.c0 == 0 && body == 0) a.iters[b] = 0;
+        if (a.csweeps && body == 0) a.csweeps[b] = 0;
+    }
+
+    // a1: nu-init of own velocity components from the history (zeros = first step)
+    double V[8][3];
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int c = 0; c < 3; ++c) V[i][c] = v[c];
+    if (live) {
+        double H[8][3];
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+#pragma unroll
+            for (int c = 0; c < 3; ++c) H[j][c] = a.hist[((int64_t)j * D + d + 3 * body + c) * B + b];
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+#pragma unroll
+            for (int c = 0; c < 3; ++c) {
+                double acc = dmul(c_nu[i][0], H[0][c]);
+#pragma unroll
+                for (int j = 1; j < 8; ++j) acc = dfma(c_nu[i][j], H[j][c], acc);
+                V[i][c] = dadd(v[c], acc);
+            }
+    }
+    const double kInf = __longlong_as_double(0x7ff0000000000000LL);
+    double m[3] = {kInf, kInf, kInf}, p[3] = {kInf, kInf, kInf};
+    int64_t n = 0, hits = 0, sweeps = 0;
+    int k = 0;
+    double Lv[8][3];
+
+    while (__any_sync(FULL, live)) {
+        ++k;
+        // ---- a2: Lq = hb o V ; Q_i = q + D(mu_i., Lq) ; Delta vs Q^[k-1] (smem) ----
+        double Lq[8][3], sLq[3], delta[3] = {0.0, 0.0, 0.0};
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+#pragma unroll
+            for (int c = 0; c < 3; ++c) Lq[j][c] = dmul(a.hb[j], V[j][c]);
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            sLq[c] = Lq[0][c];
+#pragma unroll
+            for (int j = 1; j < 8; ++j) sLq[c] = dadd(sLq[c], Lq[j][c]);
+        }
+        {
+            const double2 *M = reinterpret_cast<const double2 *>(&c_mu[0][0]);
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                double2 w[4];
+#pragma unroll
+                for (int jj = 0; jj < 4; ++jj) w[jj] = M[i * 4 + jj];
+#pragma unroll
+                for (int c = 0; c < 3; ++c) {
+                    double acc = dmul(w[0].x, Lq[0][c]);
+                    acc = dfma(w[0].y, Lq[1][c], acc);
+#pragma unroll
+                    for (int jj = 1; jj < 4; ++jj) {
+                        acc = dfma(w[jj].x, Lq[2 * jj][c], acc);
+                        acc = dfma(w[jj].y, Lq[2 * jj + 1][c], acc);
+                    }
+                    const double qn = dadd(q[c], acc);
+                    if (lane_ok) {
+                        const double e = dabs(dsub(qn, sQ[gib][i][3 * body + c]));  // unused at k = 1
+                        delta[c] = (e > delta[c]) ? e : delta[c];
+                        sQ[gib][i][3 * body + c] = qn;
+                    }
+                }
+            }
+        }
+        // ---- a5: stop test over the group's 3*NB position components (R2) ----
+        bool ok_lane = true;
+        if (k >= 2) {
+#pragma unroll
+            for (int c = 0; c < 3; ++c) {
+                const double mn = (delta[c] < p[c]) ? delta[c] : p[c];
+                const bool okc = (delta[c] == 0.0) || (m[c] <= mn);
+                m[c] = (p[c] < m[c]) ? p[c] : m[c];
+                p[c] = delta[c];
+                ok_lane = ok_lane && okc;
+            }
+        }
+        const unsigned notok = __ballot_sync(FULL, !ok_lane);
+        const bool stop = (k >= 2) && ((notok & gmask) == 0u);
+        __syncwarp();  // every body's Q^[k] is in sQ
+        // ---- a3: F_i(body) = sum over the pairs containing it, lexicographic order ----
+        const double tn1 = dadd(a.t0, dmul((double)(n0 + n), a.h));
+        (void)tn1;  // the N-body RHS is autonomous
+        bool okdiv = true;
+#pragma unroll 2
+        for (int i = 0; i < 8; ++i) {
+            const double *Qi = sQ[gib][i];
+            const double qx = Qi[3 * body], qy = Qi[3 * body + 1], qz = Qi[3 * body + 2];
+            double ax = 0.0, ay = 0.0, az = 0.0;
+#pragma unroll
+            for (int o = 0; o < NB - 1; ++o) {
+                const bool lo = o < body;          // partner j = o (j < k) or o + 1 (j > k)
+                const int j = lo ? o : o + 1;
+                const double jx = Qi[3 * j], jy = Qi[3 * j + 1], jz = Qi[3 * j + 2];
+                const double dx = lo ? dsub(qx, jx) : dsub(jx, qx);
+                const double dy = lo ? dsub(qy, jy) : dsub(jy, qy);
+                const double dz = lo ? dsub(qz, jz) : dsub(jz, qz);
+                const double r2 = dfma(dz, dz, dfma(dy, dy, dfma(dx, dx, P.eps2)));
+                const double w = ddiv_fast(P.G, dmul(r2, dsqrt_fast(r2, okdiv)), okdiv);
+                const double mw = dmul(sm[j], w);
+                const double s = lo ? -mw : mw;
+                ax = dfma(s, dx, ax);
+                ay = dfma(s, dy, ay);
+                az = dfma(s, dz, az);
+            }
+            Lv[i][0] = dmul(a.hb[i], ax);
+            Lv[i][1] = dmul(a.hb[i], ay);
+            Lv[i][2] = dmul(a.hb[i], az);
+        }
+        if (__any_sync(FULL, live && !okdiv)) {  // exact-intrinsic re-evaluation (same bits)
+#pragma unroll 1
+            for (int i = 0; i < 8; ++i) {
+                const double *Qi = sQ[gib][i];
+                const double qx = Qi[3 * body], qy = Qi[3 * body + 1], qz = Qi[3 * body + 2];
+                double ax = 0.0, ay = 0.0, az = 0.0;
+#pragma unroll
+                for (int o = 0; o < NB - 1; ++o) {
+                    const bool lo = o < body;
+                    const int j = lo ? o : o + 1;
+                    const double jx = Qi[3 * j], jy = Qi[3 * j + 1], jz = Qi[3 * j + 2];
+                    const double dx = lo ? dsub(qx, jx) : dsub(jx, qx);
+                    const double dy = lo ? dsub(qy, jy) : dsub(jy, qy);
+                    const double dz = lo ? dsub(qz, jz) : dsub(jz, qz);
+                    const double r2 = dfma(dz, dz, dfma(dy, dy, dfma(dx, dx, P.eps2)));
+                    const double w = ddiv(P.G, dmul(r2, dsqrt(r2)));
+                    const double mw = dmul(sm[j], w);
+                    const double s = lo ? -mw : mw;
+                    ax = dfma(s, dx, ax);
+                    ay = dfma(s, dy, ay);
+                    az = dfma(s, dz, az);
+                }
+                Lv[i][0] = dmul(a.hb[i], ax);
+                Lv[i][1] = dmul(a.hb[i], ay);
+                Lv[i][2] = dmul(a.hb[i], az);
+            }
+        }
+        __syncwarp();  // sQ (Q^[k]) stays for the next sweep's Delta; no writer until then
+        // ---- a6 (group finished its step): update, history, energy sample ----
+        const bool fin = live && (stop || k >= a.max_iters);
+        bool finite = true;
+        if (fin) {
+#pragma unroll
+            for (int c = 0; c < 3; ++c) {
+                double sv = Lv[0][c];
+#pragma unroll
+                for (int j = 1; j < 8; ++j) sv = dadd(sv, Lv[j][c]);
+                q[c] = dadd(q[c], sLq[c]);
+                v[c] = dadd(v[c], sv);
+                finite = finite && isfinite(q[c]) && isfinite(v[c]);
+            }
+            ++n;
+            sweeps += k;
+            hits += stop ? 0 : 1;
+        }
+        const unsigned nonfinite = __ballot_sync(FULL, fin && !finite);
+        const bool grp_bad = fin && ((nonfinite & gmask) != 0u);
+        const bool due = fin && sample && ((a.c0 + n) % a.energy_every) == 0;
+        if (__any_sync(FULL, due)) {
+            if (due) {
+#pragma unroll
+                for (int c = 0; c < 3; ++c) {
+                    sQV[gib][3 * body + c] = q[c];
+                    sQV[gib][d + 3 * body + c] = v[c];
+                }
+            }
+            __syncwarp();
+            if (due && body == 0) a.energy[((a.c0 + n) / a.energy_every) * B + b] = nbody_energy<NB>(sQV[gib], P);
+            __syncwarp();
+        }
+        if (fin && (n == a.nsteps || grp_bad)) {  // leave: history = Lv (R-4), q block zeroed
+#pragma unroll
+            for (int j = 0; j < 8; ++j)
+#pragma unroll
+                for (int c = 0; c < 3; ++c) {
+                    a.hist[((int64_t)j * D + 3 * body + c) * B + b] = 0.0;
+                    a.hist[((int64_t)j * D + d + 3 * body + c) * B + b] = Lv[j][c];
+                }
+            if (grp_bad) bad = n0 + n;
+            live = false;
+        }
+        if (fin) {
+            k = 0;
+#pragma unroll
+            for (int c = 0; c < 3; ++c) m[c] = p[c] = kInf;
+        }
+        // ---- a4 / next step's a1: V_i = v + D(W_i., Lv), W = fin ? nu : mu ----
+        {
+            const double2 *W = reinterpret_cast<const double2 *>(&sW[fin ? 1 : 0][0]);
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                double2 w[4];
+#pragma unroll
+                for (int jj = 0; jj < 4; ++jj) w[jj] = W[i * 4 + jj];
+#pragma unroll
+                for (int c = 0; c < 3; ++c) {
+                    double acc = dmul(w[0].x, Lv[0][c]);
+                    acc = dfma(w[0].y, Lv[1][c], acc);
+#pragma unroll
+                    for (int jj = 1; jj < 4; ++jj) {
+                        acc = dfma(w[jj].x, Lv[2 * jj][c], acc);
+                        acc = dfma(w[jj].y, Lv[2 * jj + 1][c], acc);
+                    }
+                    V[i][c] = dadd(v[c], acc);
+                }
+            }
+        }
+    }
+    if (valid) {
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            a.y[(int64_t)(3 * body + c) * B + b] = q[c];
+            a.y[(int64_t)(d + 3 * body + c) * B + b] = v[c];
+        }
+        if (body == 0) {
+            if (a.nsteps > 0 && a.stats[1 * B + b] == 0) {
+                a.stats[0 * B + b] += hits;
+                a.stats[1 * B + b] = bad;
+                a.stats[2 * B + b] += sweeps;
+                if (a.iters) a.iters[b] = (a.c0 == 0) ? sweeps : a.iters[b] + sweeps;
+                if (a.csweeps) a.csweeps[b] = (int32_t)sweeps;
+            }
+        }
+    }
+}
+
+}  // namespace irk

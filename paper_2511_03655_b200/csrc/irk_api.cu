@@ -12,6 +12,7 @@
 #include "../../include/irk.h"
 #include "balance.cuh"
 #include "ensemble_g1.cuh"
+#include "ensemble_nbody.cuh"
 #include "problems.cuh"
 #include "tableau.h"
 
@@ -95,14 +96,15 @@ __global__ void advance_n_kernel(int64_t *n_done, int64_t nsteps) { *n_done += n
 struct Sched {
     int32_t *perm, *csweeps, *sorted, *bins;
 };
-int64_t g1_slots(int64_t B) { return (B + irk::G1_THREADS - 1) / irk::G1_THREADS * irk::G1_THREADS; }
+// thread-slot capacity of the scheduler's permutation (>= slots of any ensemble kernel)
+int64_t perm_slots(int64_t B) { return (B + 63) / 64 * 64; }
 size_t sched_bytes(const irk_ctx *c) {
-    return sizeof(int32_t) * ((size_t)g1_slots(c->batch) + 2 * (size_t)c->batch + irk::kCostBins);
+    return sizeof(int32_t) * ((size_t)perm_slots(c->batch) + 2 * (size_t)c->batch + irk::kCostBins);
 }
 Sched sched_of(const irk_ctx *c, char *ws) {
     Sched s;
     s.perm = reinterpret_cast<int32_t *>(ws + kHeader + hist_bytes(c) + stats_bytes(c));
-    s.csweeps = s.perm + g1_slots(c->batch);
+    s.csweeps = s.perm + perm_slots(c->batch);
     s.sorted = s.csweeps + c->batch;
     s.bins = s.sorted + c->batch;
     return s;
@@ -117,33 +119,22 @@ int64_t balance_chunk(const irk_ctx *c) {
     return ch < c->nsteps ? ch : 0;
 }
 
-template <class P>
-int launch_g1(irk_ctx *c, const P &prob, double *y, double t0, char *ws, double *energy,
-              int64_t *iters, cudaStream_t st) {
-    EnsArgs a;
-    for (int j = 0; j < 8; ++j) a.hb[j] = c->T.hb[j];
-    a.y = y;
-    a.n_done = reinterpret_cast<const int64_t *>(ws);
-    a.hist = reinterpret_cast<double *>(ws + kHeader);
-    a.stats = reinterpret_cast<int64_t *>(ws + kHeader + hist_bytes(c));
-    a.energy = energy;
-    a.iters = iters;
-    a.batch = c->batch;
-    a.energy_every = c->energy_every;
-    a.h = c->h;
-    a.t0 = t0;
-    a.max_iters = c->max_iters;
-    const int threads = irk::G1_THREADS;
-    const int64_t blocks = (c->batch + threads - 1) / threads;
+// Runs the call's nsteps in (cost-balanced) chunks.  `launch(args, nblocks)` starts
+// one ensemble kernel over `nblocks` blocks; a block holds `wpb` warps of `spw`
+// trajectory slots each.
+template <class LaunchFn>
+int run_chunks(irk_ctx *c, EnsArgs &a, char *ws, int64_t nblocks, int wpb, int spw, cudaStream_t st,
+               LaunchFn launch) {
     const int64_t chunk = balance_chunk(c);
-    if (chunk == 0) {  // single launch over all steps, identity assignment
+    const int64_t nslots = nblocks * wpb * spw;
+    if (chunk == 0) {  // one launch over all steps, identity assignment
         a.nsteps = c->nsteps;
         a.c0 = 0;
-        a.perm = nullptr;
         a.csweeps = nullptr;
+        a.perm = nullptr;
         a.nslots = c->batch;
-        irk::ens_g1_kernel<P><<<(unsigned)blocks, threads, 0, st>>>(a, prob);
-        int rc = cuda_check(c, cudaGetLastError(), "ens_g1_kernel launch");
+        launch(a, nblocks);
+        int rc = cuda_check(c, cudaGetLastError(), "ensemble kernel launch");
         if (rc) return rc;
         advance_n_kernel<<<1, 1, 0, st>>>(reinterpret_cast<int64_t *>(ws), c->nsteps);
         return cuda_check(c, cudaGetLastError(), "advance_n launch");
@@ -163,19 +154,89 @@ int launch_g1(irk_ctx *c, const P &prob, double *y, double t0, char *ws, double 
             irk::cost_hist_kernel<<<sb, 256, 0, st>>>(sc.csweeps, c->batch, chunk, sc.bins);
             irk::cost_scan_kernel<<<1, irk::kCostBins, 0, st>>>(sc.bins);
             irk::cost_scatter_kernel<<<sb, 256, 0, st>>>(sc.csweeps, c->batch, chunk, sc.bins, sc.sorted);
-            const int64_t nslots = g1_slots(c->batch);
-            irk::cost_perm_kernel<<<(unsigned)((nslots + 255) / 256), 256, 0, st>>>(sc.sorted, c->batch, blocks,
-                                                                                      threads, sc.perm);
+            irk::cost_perm_kernel<<<(unsigned)((nslots + 255) / 256), 256, 0, st>>>(sc.sorted, c->batch, nblocks, wpb,
+                                                                                      spw, sc.perm);
             a.perm = sc.perm;
             a.nslots = nslots;
         }
-        irk::ens_g1_kernel<P><<<(unsigned)blocks, threads, 0, st>>>(a, prob);
-        int rc = cuda_check(c, cudaGetLastError(), "ens_g1_kernel launch");
+        launch(a, nblocks);
+        int rc = cuda_check(c, cudaGetLastError(), "ensemble kernel launch");
         if (rc) return rc;
         advance_n_kernel<<<1, 1, 0, st>>>(reinterpret_cast<int64_t *>(ws), steps);
         if ((rc = cuda_check(c, cudaGetLastError(), "advance_n launch"))) return rc;
     }
     return IRK_OK;
+}
+
+EnsArgs ens_args(irk_ctx *c, double *y, double t0, char *ws, double *energy, int64_t *iters) {
+    EnsArgs a;
+    for (int j = 0; j < 8; ++j) a.hb[j] = c->T.hb[j];
+    a.y = y;
+    a.n_done = reinterpret_cast<const int64_t *>(ws);
+    a.hist = reinterpret_cast<double *>(ws + kHeader);
+    a.stats = reinterpret_cast<int64_t *>(ws + kHeader + hist_bytes(c));
+    a.energy = energy;
+    a.iters = iters;
+    a.batch = c->batch;
+    a.energy_every = c->energy_every;
+    a.h = c->h;
+    a.t0 = t0;
+    a.max_iters = c->max_iters;
+    return a;
+}
+
+template <class P>
+int launch_g1(irk_ctx *c, const P &prob, double *y, double t0, char *ws, double *energy,
+              int64_t *iters, cudaStream_t st) {
+    EnsArgs a = ens_args(c, y, t0, ws, energy, iters);
+    const int64_t blocks = (c->batch + irk::G1_THREADS - 1) / irk::G1_THREADS;
+    return run_chunks(c, a, ws, blocks, irk::G1_THREADS / 32, 32, st, [&](const EnsArgs &aa, int64_t nb) {
+        irk::ens_g1_kernel<P><<<(unsigned)nb, irk::G1_THREADS, 0, st>>>(aa, prob);
+    });
+}
+
+template <int NB>
+int launch_nbody_t(irk_ctx *c, double *y, double t0, char *ws, double *energy, int64_t *iters, cudaStream_t st) {
+    irk::NBodyParams P;
+    P.G = c->params[0];
+    P.eps2 = c->params[1] * c->params[1];
+    for (int i = 0; i < 16; ++i) P.m[i] = i < NB ? c->params[2 + i] : 0.0;
+    EnsArgs a = ens_args(c, y, t0, ws, energy, iters);
+    constexpr int GPW = 32 / NB, WPB = irk::NB_THREADS / 32;
+    const int64_t blocks = (c->batch + GPW * WPB - 1) / (GPW * WPB);
+    return run_chunks(c, a, ws, blocks, WPB, GPW, st, [&](const EnsArgs &aa, int64_t nb) {
+        irk::ens_nbody_kernel<NB><<<(unsigned)nb, irk::NB_THREADS, 0, st>>>(aa, P);
+    });
+}
+
+int launch_nbody(irk_ctx *c, double *y, double t0, char *ws, double *energy, int64_t *iters, cudaStream_t st) {
+    switch (c->dim / 6) {
+    case 2: return launch_nbody_t<2>(c, y, t0, ws, energy, iters, st);
+    case 3: return launch_nbody_t<3>(c, y, t0, ws, energy, iters, st);
+    case 4: return launch_nbody_t<4>(c, y, t0, ws, energy, iters, st);
+    case 5: return launch_nbody_t<5>(c, y, t0, ws, energy, iters, st);
+    case 6: return launch_nbody_t<6>(c, y, t0, ws, energy, iters, st);
+    case 8: return launch_nbody_t<8>(c, y, t0, ws, energy, iters, st);
+    }
+    return fail(c, IRK_E_ARG, "irk_integrate: IRK_NBODY ensembles support N in {2,3,4,5,6,8} bodies");
+}
+
+template <int NB>
+__global__ void energy_nbody_kernel(const double *y, double *H, int64_t B, const __grid_constant__ irk::NBodyParams P) {
+    int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (b >= B) return;
+    double qv[6 * NB];
+    for (int l = 0; l < 6 * NB; ++l) qv[l] = y[l * B + b];
+    H[b] = irk::nbody_energy<NB>(qv, P);
+}
+
+template <int NB>
+void launch_energy_nbody_t(irk_ctx *c, const double *y, double *H, cudaStream_t st) {
+    irk::NBodyParams P;
+    P.G = c->params[0];
+    P.eps2 = c->params[1] * c->params[1];
+    for (int i = 0; i < 16; ++i) P.m[i] = i < NB ? c->params[2 + i] : 0.0;
+    energy_nbody_kernel<NB><<<(unsigned)((c->batch + 127) / 128), 128, 0, st>>>(y, H, c->batch, P);
 }
 
 template <class P>
@@ -209,10 +270,15 @@ irk_ctx *irk_create(int problem, int dim, double h, int64_t nsteps, int64_t batc
     case IRK_FPU_BETA:
         if (dim < 2 || dim % 2) return bad("irk_create: FPU needs an even dim >= 2");
         return bad("irk_create: IRK_FPU_BETA kernel not built yet");
-    case IRK_NBODY:
+    case IRK_NBODY: {
+        if (dim % 6 || dim < 12) return bad("irk_create: N-body needs dim = 6N, N >= 2");
+        const int N = dim / 6;
+        if (N > 6 && N != 8) return bad("irk_create: IRK_NBODY ensembles support N in {2,...,6, 8}");
+        break;
+    }
     case IRK_NBODY_DIRECT:
         if (dim % 6 || dim < 12) return bad("irk_create: N-body needs dim = 6N, N >= 2");
-        return bad("irk_create: N-body kernels not built yet");
+        return bad("irk_create: IRK_NBODY_DIRECT kernels not built yet");
     default: return bad("irk_create: unknown problem");
     }
     if (!std::isfinite(h) || h == 0.0) return bad("irk_create: h must be finite and nonzero");
@@ -298,6 +364,9 @@ int irk_integrate(irk_ctx *c, double *y, double t0, void *workspace, double *ene
         rc = launch_g1(c, P, y, t0, ws, energy, iters, st);
         break;
     }
+    case IRK_NBODY:
+        rc = launch_nbody(c, y, t0, ws, energy, iters, st);
+        break;
     default: return fail(c, IRK_E_ARG, "irk_integrate: problem not supported");
     }
     return rc;
@@ -369,6 +438,17 @@ int irk_energy(irk_ctx *c, const double *y, double *H, void *stream) {
         break;
     case IRK_HENON_HEILES:
         energy_g1_kernel<<<blocks, threads, 0, st>>>(y, H, c->batch, irk::HenonHeiles{c->params[0], c->params[1]});
+        break;
+    case IRK_NBODY:
+        switch (c->dim / 6) {
+        case 2: launch_energy_nbody_t<2>(c, y, H, st); break;
+        case 3: launch_energy_nbody_t<3>(c, y, H, st); break;
+        case 4: launch_energy_nbody_t<4>(c, y, H, st); break;
+        case 5: launch_energy_nbody_t<5>(c, y, H, st); break;
+        case 6: launch_energy_nbody_t<6>(c, y, H, st); break;
+        case 8: launch_energy_nbody_t<8>(c, y, H, st); break;
+        default: return fail(c, IRK_E_ARG, "irk_energy: unsupported N");
+        }
         break;
     default: return fail(c, IRK_E_ARG, "irk_energy: problem not supported");
     }

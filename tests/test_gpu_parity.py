@@ -233,3 +233,54 @@ def test_cost_balanced_schedule_is_bitwise_neutral(irk, orc):
     assert np.array_equal(outs[1][0][:, idx], orr["y"])
     assert np.array_equal(outs[1][1][:, idx], orr["energy"])
     assert np.array_equal(outs[1][2][idx], orr["iters"])
+
+
+# ------------------------------------------------------------------ config 3
+def test_config3_six_body_ragged_energy(irk, orc):
+    """Config-3 generator, ragged batch of 37 members, 3,000 steps, energy every
+    250 steps; body-per-lane kernel vs oracle, bitwise."""
+    w = wl.six_body_ensemble(batch=37, nsteps=3000)
+    g = run_gpu(irk, w, energy_every=250)
+    o = orc.integrate(w.problem, w.y, w.params, w.h, w.nsteps, energy_every=250)
+    assert_parity(g, o, energy=True)
+
+
+def test_config3_full_length_subset(irk, orc):
+    """Config 3 at full length (50,000 steps) on 48 members, bitwise."""
+    w = wl.six_body_ensemble(batch=48)
+    g = run_gpu(irk, w)
+    o = orc.integrate(w.problem, w.y, w.params, w.h, w.nsteps)
+    assert_parity(g, o)
+
+
+def test_config3_full_batch_sampled(irk, orc):
+    """Config 3 at full batch (16,384 members) in the bench's launch
+    configuration (cost-balanced chunks), 2,000 steps; oracle on 40 sampled members."""
+    w = wl.six_body_ensemble(nsteps=2000)
+    g = run_gpu(irk, w)
+    idx = np.linspace(0, w.batch - 1, 40).astype(int)
+    o = orc.integrate(w.problem, w.y[:, idx], w.params, w.h, w.nsteps)
+    assert_parity(dict(y=g["y"][:, idx], iters=g["iters"][idx]), o)
+
+
+def test_nbody_small_n_variants(irk, orc):
+    """Other group sizes of the body-per-lane kernel (N = 2, 3, 5): random
+    softened systems, bitwise."""
+    rng = np.random.default_rng(3)
+    for N in (2, 3, 5):
+        B = 23
+        q = rng.standard_normal((3 * N, B))
+        v = 0.3 * rng.standard_normal((3 * N, B))
+        params = np.concatenate([[1.0, 0.05], rng.uniform(0.2, 1.0, N)])
+        w = wl.Workload(f"nb{N}", wl.NBODY, 6 * N, np.concatenate([q, v]), params, 0.01, 300)
+        g = run_gpu(irk, w, energy_every=100)
+        o = orc.integrate(w.problem, w.y, w.params, w.h, w.nsteps, energy_every=100)
+        assert_parity(g, o, energy=True)
+
+
+def test_nbody_energy_entry_point(irk, orc):
+    w = wl.six_body_ensemble(batch=50)
+    with irk.Integrator(w.problem, w.dim, w.h, 1, w.batch, w.params) as ig:
+        H = ig.energy(torch.tensor(w.y, device="cuda")).cpu().numpy()
+    Ho = np.array([orc.energy(w.problem, w.dim, w.params, w.y[:, b]) for b in range(w.batch)])
+    assert np.array_equal(H, Ho)

@@ -63,6 +63,7 @@ def test_library_tableau_bitwise_equals_oracle_and_mpmath(irk, orc):
     (1, 4, 0.1, 10, 0),          # batch < 1
     (9, 4, 0.1, 10, 4),          # unknown problem
     (2, 13, 0.1, 10, 4),         # N-body dim % 6
+    (2, 42, 0.1, 10, 4),         # N-body ensembles: N = 7 unsupported
     (3, 7, 0.1, 10, 4),          # FPU odd dim
 ])
 def test_create_argument_errors(irk, args):
