@@ -1,0 +1,247 @@
+// Ensemble kernel, mapping "site-per-lane" (config 4, FPU-beta chains): one warp
+// per chain of N = 32*SPL sites, lane L owns sites L*SPL .. L*SPL+SPL-1 (their
+// positions and velocities for all 8 stages).
+//
+// Both 8x8 contractions are thread-local (components are independent); the
+// RHS of a site needs its neighbours' stage positions, read from a shared-memory
+// copy of Q^[k] that also serves as Q^[k-1] for the stop test.  A warp is one
+// trajectory, so the sweep loop has no divergence at all; the stop test is a
+// warp vote.
+//
+// Canonical RHS (oracle accel_fpu): bond b
+// (b = 0..N, q_{-1} = q_N = 0 in 0-based sites) has D_b = q_b - q_{b-1} and
+// f_b = fma(beta*(D_b*D_b), D_b, D_b); site s gets a_s = f_{s+1} - f_s.  A bond
+// shared by two lanes is evaluated by both with identical operations.
+#pragma once
+#include <cstdint>
+
+#include "ens_common.cuh"
+#include "fp64.cuh"
+
+namespace irk {
+
+constexpr int CH_THREADS = 64;  // 2 chains per block
+
+__device__ __forceinline__ double fpu_bond(double dl, double beta) {
+    return dfma(dmul(beta, dmul(dl, dl)), dl, dl);
+}
+
+// H = sum p^2/2 + sum_b (D^2/2 + beta D^4/4), Neumaier, canonical order (oracle).
+template <int N>
+__device__ double fpu_energy(const double *q, const double *v, double beta) {
+    Neumaier n;
+    for (int i = 0; i < N; ++i) n.add(dmul(0.5, dmul(v[i], v[i])));
+    for (int bnd = 0; bnd <= N; ++bnd) {
+        const double ql = (bnd == 0) ? 0.0 : q[bnd - 1];
+        const double qr = (bnd == N) ? 0.0 : q[bnd];
+        const double dl = dsub(qr, ql);
+        const double d2 = dmul(dl, dl);
+        n.add(dadd(dmul(0.5, d2), dmul(dmul(0.25, beta), dmul(d2, d2))));
+    }
+    return n.result();
+}
+
+template <int SPL>
+__global__ void __launch_bounds__(CH_THREADS) ens_chain_kernel(const __grid_constant__ EnsArgs a, const double beta) {
+    constexpr int N = 32 * SPL, d = N, D = 2 * N, CPB = CH_THREADS / 32;
+    const unsigned FULL = 0xffffffffu;
+    const int64_t B = a.batch;
+    __shared__ __align__(16) double sW[2][64];
+    __shared__ double sQ[CPB][8][N];   // Q^[k] of the chain (neighbour reads + Delta)
+    __shared__ double sQV[CPB][2 * N]; // (q, v) for energy samples
+    for (int e = threadIdx.x; e < 128; e += blockDim.x)
+        sW[e >> 6][e & 63] = (e < 64) ? (&c_mu[0][0])[e] : (&c_nu[0][0])[e - 64];
+    __syncthreads();
+    const int lane = threadIdx.x & 31, cib = threadIdx.x >> 5;
+    const int64_t slot = (int64_t)blockIdx.x * CPB + cib;
+    if (slot >= a.nslots) return;  // warp-uniform
+    const int64_t b = a.perm ? (int64_t)a.perm[slot] : slot;
+    if (b < 0 || b >= B) return;   // warp-uniform
+    const int s0 = lane * SPL;
+
+    double q[SPL], v[SPL];
+#pragma unroll
+    for (int s = 0; s < SPL; ++s) {
+        q[s] = a.y[(int64_t)(s0 + s) * B + b];
+        v[s] = a.y[(int64_t)(d + s0 + s) * B + b];
+    }
+    int64_t bad = a.stats[1 * B + b];
+    const int64_t n0 = *a.n_done;
+    const bool sample = (a.energy != nullptr) && (a.energy_every > 0);
+    auto energy_sample = [&](int64_t idx) {
+#pragma unroll
+        for (int s = 0; s < SPL; ++s) {
+            sQV[cib][s0 + s] = q[s];
+            sQV[cib][N + s0 + s] = v[s];
+        }
+        __syncwarp();
+        if (lane == 0) a.energy[idx * B + b] = fpu_energy<N>(sQV[cib], sQV[cib] + N, beta);
+        __syncwarp();
+    };
+    if (sample && a.c0 == 0) energy_sample(0);
+    if (bad > 0 || a.nsteps == 0) {
+        if (lane == 0) {
+            if (a.iters && a.c0 == 0) a.iters[b] = 0;
+            if (a.csweeps) a.csweeps[b] = 0;
+        }
+        return;
+    }
+    double V[8][SPL];
+    {
+        double H[8][SPL];
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+#pragma unroll
+            for (int s = 0; s < SPL; ++s) H[j][s] = a.hist[((int64_t)j * D + d + s0 + s) * B + b];
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+#pragma unroll
+            for (int s = 0; s < SPL; ++s) {
+                double acc = dmul(c_nu[i][0], H[0][s]);
+#pragma unroll
+                for (int j = 1; j < 8; ++j) acc = dfma(c_nu[i][j], H[j][s], acc);
+                V[i][s] = dadd(v[s], acc);
+            }
+    }
+    const double kInf = __longlong_as_double(0x7ff0000000000000LL);
+    double m[SPL], p[SPL];
+#pragma unroll
+    for (int s = 0; s < SPL; ++s) m[s] = p[s] = kInf;
+    int64_t n = 0, hits = 0, sweeps = 0;
+    int k = 0;
+    while (n < a.nsteps) {  // warp-uniform
+        ++k;
+        // a2 + Delta
+        double Lq[8][SPL], sLq[SPL], delta[SPL];
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+#pragma unroll
+            for (int s = 0; s < SPL; ++s) Lq[j][s] = dmul(a.hb[j], V[j][s]);
+#pragma unroll
+        for (int s = 0; s < SPL; ++s) {
+            sLq[s] = Lq[0][s];
+#pragma unroll
+            for (int j = 1; j < 8; ++j) sLq[s] = dadd(sLq[s], Lq[j][s]);
+            delta[s] = 0.0;
+        }
+        __syncwarp();  // previous sweep's neighbour reads of sQ are done
+        {
+            const double2 *M = reinterpret_cast<const double2 *>(&c_mu[0][0]);
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                double2 w[4];
+#pragma unroll
+                for (int jj = 0; jj < 4; ++jj) w[jj] = M[i * 4 + jj];
+#pragma unroll
+                for (int s = 0; s < SPL; ++s) {
+                    double acc = dmul(w[0].x, Lq[0][s]);
+                    acc = dfma(w[0].y, Lq[1][s], acc);
+#pragma unroll
+                    for (int jj = 1; jj < 4; ++jj) {
+                        acc = dfma(w[jj].x, Lq[2 * jj][s], acc);
+                        acc = dfma(w[jj].y, Lq[2 * jj + 1][s], acc);
+                    }
+                    const double qn = dadd(q[s], acc);
+                    const double e = dabs(dsub(qn, sQ[cib][i][s0 + s]));
+                    delta[s] = (e > delta[s]) ? e : delta[s];
+                    sQ[cib][i][s0 + s] = qn;
+                }
+            }
+        }
+        bool ok_lane = true;
+        if (k >= 2) {
+#pragma unroll
+            for (int s = 0; s < SPL; ++s) {
+                const double mn = (delta[s] < p[s]) ? delta[s] : p[s];
+                const bool oks = (delta[s] == 0.0) || (m[s] <= mn);
+                m[s] = (p[s] < m[s]) ? p[s] : m[s];
+                p[s] = delta[s];
+                ok_lane = ok_lane && oks;
+            }
+        }
+        const bool stop = (k >= 2) && __all_sync(FULL, ok_lane);
+        __syncwarp();
+        // a3: bond forces of the lane's sites for every stage
+        double Lv[8][SPL];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            const double *Qi = sQ[cib][i];
+            double qs[SPL + 2];
+            qs[0] = (s0 == 0) ? 0.0 : Qi[s0 - 1];
+#pragma unroll
+            for (int s = 0; s < SPL; ++s) qs[s + 1] = Qi[s0 + s];
+            qs[SPL + 1] = (s0 + SPL == N) ? 0.0 : Qi[s0 + SPL];
+            double f[SPL + 1];
+#pragma unroll
+            for (int t = 0; t <= SPL; ++t) f[t] = fpu_bond(dsub(qs[t + 1], qs[t]), beta);
+#pragma unroll
+            for (int s = 0; s < SPL; ++s) Lv[i][s] = dmul(a.hb[i], dsub(f[s + 1], f[s]));
+        }
+        const bool fin = stop || (k >= a.max_iters);
+        if (fin) {
+            bool finite = true;
+#pragma unroll
+            for (int s = 0; s < SPL; ++s) {
+                double sv = Lv[0][s];
+#pragma unroll
+                for (int j = 1; j < 8; ++j) sv = dadd(sv, Lv[j][s]);
+                q[s] = dadd(q[s], sLq[s]);
+                v[s] = dadd(v[s], sv);
+                finite = finite && isfinite(q[s]) && isfinite(v[s]);
+            }
+            finite = __all_sync(FULL, finite);
+            ++n;
+            sweeps += k;
+            hits += stop ? 0 : 1;
+            k = 0;
+#pragma unroll
+            for (int s = 0; s < SPL; ++s) m[s] = p[s] = kInf;
+            if (sample && ((a.c0 + n) % a.energy_every) == 0) energy_sample((a.c0 + n) / a.energy_every);
+            if (n == a.nsteps || !finite) {
+#pragma unroll
+                for (int j = 0; j < 8; ++j)
+#pragma unroll
+                    for (int s = 0; s < SPL; ++s) {
+                        a.hist[((int64_t)j * D + s0 + s) * B + b] = 0.0;
+                        a.hist[((int64_t)j * D + d + s0 + s) * B + b] = Lv[j][s];
+                    }
+                if (!finite) bad = n0 + n;
+                break;
+            }
+        }
+        {
+            const double2 *W = reinterpret_cast<const double2 *>(&sW[fin ? 1 : 0][0]);
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                double2 w[4];
+#pragma unroll
+                for (int jj = 0; jj < 4; ++jj) w[jj] = W[i * 4 + jj];
+#pragma unroll
+                for (int s = 0; s < SPL; ++s) {
+                    double acc = dmul(w[0].x, Lv[0][s]);
+                    acc = dfma(w[0].y, Lv[1][s], acc);
+#pragma unroll
+                    for (int jj = 1; jj < 4; ++jj) {
+                        acc = dfma(w[jj].x, Lv[2 * jj][s], acc);
+                        acc = dfma(w[jj].y, Lv[2 * jj + 1][s], acc);
+                    }
+                    V[i][s] = dadd(v[s], acc);
+                }
+            }
+        }
+    }
+#pragma unroll
+    for (int s = 0; s < SPL; ++s) {
+        a.y[(int64_t)(s0 + s) * B + b] = q[s];
+        a.y[(int64_t)(d + s0 + s) * B + b] = v[s];
+    }
+    if (lane == 0) {
+        a.stats[0 * B + b] += hits;
+        a.stats[1 * B + b] = bad;
+        a.stats[2 * B + b] += sweeps;
+        if (a.iters) a.iters[b] = (a.c0 == 0) ? sweeps : a.iters[b] + sweeps;
+        if (a.csweeps) a.csweeps[b] = (int32_t)sweeps;
+    }
+}
+
+}  // namespace irk

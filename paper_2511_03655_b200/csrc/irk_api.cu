@@ -13,6 +13,7 @@
 #include "balance.cuh"
 #include "ensemble_g1.cuh"
 #include "ensemble_nbody.cuh"
+#include "ensemble_chain.cuh"
 #include "problems.cuh"
 #include "tableau.h"
 
@@ -209,6 +210,26 @@ int launch_nbody_t(irk_ctx *c, double *y, double t0, char *ws, double *energy, i
     });
 }
 
+template <int SPL>
+int launch_chain_t(irk_ctx *c, double *y, double t0, char *ws, double *energy, int64_t *iters, cudaStream_t st) {
+    EnsArgs a = ens_args(c, y, t0, ws, energy, iters);
+    constexpr int CPB = irk::CH_THREADS / 32;
+    const int64_t blocks = (c->batch + CPB - 1) / CPB;
+    const double beta = c->params[0];
+    return run_chunks(c, a, ws, blocks, CPB, 1, st, [&](const EnsArgs &aa, int64_t nb) {
+        irk::ens_chain_kernel<SPL><<<(unsigned)nb, irk::CH_THREADS, 0, st>>>(aa, beta);
+    });
+}
+
+int launch_chain(irk_ctx *c, double *y, double t0, char *ws, double *energy, int64_t *iters, cudaStream_t st) {
+    switch (c->dim / 2) {
+    case 32: return launch_chain_t<1>(c, y, t0, ws, energy, iters, st);
+    case 64: return launch_chain_t<2>(c, y, t0, ws, energy, iters, st);
+    case 128: return launch_chain_t<4>(c, y, t0, ws, energy, iters, st);
+    }
+    return fail(c, IRK_E_ARG, "irk_integrate: IRK_FPU_BETA supports N in {32, 64, 128} sites");
+}
+
 int launch_nbody(irk_ctx *c, double *y, double t0, char *ws, double *energy, int64_t *iters, cudaStream_t st) {
     switch (c->dim / 6) {
     case 2: return launch_nbody_t<2>(c, y, t0, ws, energy, iters, st);
@@ -219,6 +240,18 @@ int launch_nbody(irk_ctx *c, double *y, double t0, char *ws, double *energy, int
     case 8: return launch_nbody_t<8>(c, y, t0, ws, energy, iters, st);
     }
     return fail(c, IRK_E_ARG, "irk_integrate: IRK_NBODY ensembles support N in {2,3,4,5,6,8} bodies");
+}
+
+template <int N>
+__global__ void energy_fpu_kernel(const double *y, double *H, int64_t B, double beta) {
+    int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (b >= B) return;
+    double q[N], v[N];
+    for (int l = 0; l < N; ++l) {
+        q[l] = y[l * B + b];
+        v[l] = y[(N + l) * B + b];
+    }
+    H[b] = irk::fpu_energy<N>(q, v, beta);
 }
 
 template <int NB>
@@ -269,7 +302,9 @@ irk_ctx *irk_create(int problem, int dim, double h, int64_t nsteps, int64_t batc
         break;
     case IRK_FPU_BETA:
         if (dim < 2 || dim % 2) return bad("irk_create: FPU needs an even dim >= 2");
-        return bad("irk_create: IRK_FPU_BETA kernel not built yet");
+        if (dim / 2 != 32 && dim / 2 != 64 && dim / 2 != 128)
+            return bad("irk_create: IRK_FPU_BETA supports N in {32, 64, 128} sites (one warp per chain)");
+        break;
     case IRK_NBODY: {
         if (dim % 6 || dim < 12) return bad("irk_create: N-body needs dim = 6N, N >= 2");
         const int N = dim / 6;
@@ -367,6 +402,9 @@ int irk_integrate(irk_ctx *c, double *y, double t0, void *workspace, double *ene
     case IRK_NBODY:
         rc = launch_nbody(c, y, t0, ws, energy, iters, st);
         break;
+    case IRK_FPU_BETA:
+        rc = launch_chain(c, y, t0, ws, energy, iters, st);
+        break;
     default: return fail(c, IRK_E_ARG, "irk_integrate: problem not supported");
     }
     return rc;
@@ -439,6 +477,16 @@ int irk_energy(irk_ctx *c, const double *y, double *H, void *stream) {
     case IRK_HENON_HEILES:
         energy_g1_kernel<<<blocks, threads, 0, st>>>(y, H, c->batch, irk::HenonHeiles{c->params[0], c->params[1]});
         break;
+    case IRK_FPU_BETA: {
+        const unsigned nb = (unsigned)((c->batch + 127) / 128);
+        switch (c->dim / 2) {
+        case 32: energy_fpu_kernel<32><<<nb, 128, 0, st>>>(y, H, c->batch, c->params[0]); break;
+        case 64: energy_fpu_kernel<64><<<nb, 128, 0, st>>>(y, H, c->batch, c->params[0]); break;
+        case 128: energy_fpu_kernel<128><<<nb, 128, 0, st>>>(y, H, c->batch, c->params[0]); break;
+        default: return fail(c, IRK_E_ARG, "irk_energy: unsupported N");
+        }
+        break;
+    }
     case IRK_NBODY:
         switch (c->dim / 6) {
         case 2: launch_energy_nbody_t<2>(c, y, H, st); break;

@@ -284,3 +284,44 @@ def test_nbody_energy_entry_point(irk, orc):
         H = ig.energy(torch.tensor(w.y, device="cuda")).cpu().numpy()
     Ho = np.array([orc.energy(w.problem, w.dim, w.params, w.y[:, b]) for b in range(w.batch)])
     assert np.array_equal(H, Ho)
+
+
+# ------------------------------------------------------------------ config 4
+def test_config4_fpu_ragged_energy(irk, orc):
+    """Config-4 generator (N = 64, beta = 1, h = 0.1), 19 chains, 4,000 steps,
+    energy every 500; site-per-lane kernel vs oracle, bitwise."""
+    w = wl.fpu_ensemble(batch=19, nsteps=4000)
+    g = run_gpu(irk, w, energy_every=500)
+    o = orc.integrate(w.problem, w.y, w.params, w.h, w.nsteps, energy_every=500)
+    assert_parity(g, o, energy=True)
+
+
+def test_config4_full_length_subset(irk, orc):
+    """Config 4 at full length (100,000 steps) on 16 chains, bitwise."""
+    w = wl.fpu_ensemble(batch=16)
+    g = run_gpu(irk, w)
+    o = orc.integrate(w.problem, w.y, w.params, w.h, w.nsteps)
+    assert_parity(g, o)
+
+
+def test_config4_full_batch_sampled(irk, orc):
+    """Config 4 at full batch (4,096 chains), 3,000 steps, cost-balanced chunks;
+    oracle on 24 sampled chains."""
+    w = wl.fpu_ensemble(nsteps=3000)
+    g = run_gpu(irk, w)
+    idx = np.linspace(0, w.batch - 1, 24).astype(int)
+    o = orc.integrate(w.problem, w.y[:, idx], w.params, w.h, w.nsteps)
+    assert_parity(dict(y=g["y"][:, idx], iters=g["iters"][idx]), o)
+
+
+def test_fpu_other_sizes_and_energy_entry(irk, orc):
+    for N in (32, 128):
+        w = wl.fpu_ensemble(batch=5, nsteps=500, N=N)
+        g = run_gpu(irk, w, energy_every=100)
+        o = orc.integrate(w.problem, w.y, w.params, w.h, w.nsteps, energy_every=100)
+        assert_parity(g, o, energy=True)
+    w = wl.fpu_ensemble(batch=33)
+    with irk.Integrator(w.problem, w.dim, w.h, 1, w.batch, w.params) as ig:
+        H = ig.energy(torch.tensor(w.y, device="cuda")).cpu().numpy()
+    Ho = np.array([orc.energy(w.problem, w.dim, w.params, w.y[:, b]) for b in range(w.batch)])
+    assert np.array_equal(H, Ho)

@@ -65,6 +65,7 @@ def test_library_tableau_bitwise_equals_oracle_and_mpmath(irk, orc):
     (2, 13, 0.1, 10, 4),         # N-body dim % 6
     (2, 42, 0.1, 10, 4),         # N-body ensembles: N = 7 unsupported
     (3, 7, 0.1, 10, 4),          # FPU odd dim
+    (3, 40, 0.1, 10, 4),         # FPU: N must be 32, 64 or 128 (one warp per chain)
 ])
 def test_create_argument_errors(irk, args):
     with pytest.raises(irk.IrkError):
