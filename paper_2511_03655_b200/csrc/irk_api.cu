@@ -14,6 +14,7 @@
 #include "ensemble_g1.cuh"
 #include "ensemble_nbody.cuh"
 #include "ensemble_chain.cuh"
+#include "nbody_direct.cuh"
 #include "problems.cuh"
 #include "tableau.h"
 
@@ -39,6 +40,9 @@ struct irk_ctx {
     void *d_ws = nullptr;
     size_t cap_y = 0, cap_energy = 0, cap_ws = 0;
     int64_t cap_iters = 0;
+    // large-N path
+    double *d_mass = nullptr, *d_rows = nullptr;
+    irk::NbdCtl *h_ctl = nullptr;  // pinned readback of the control block
 };
 
 namespace {
@@ -167,6 +171,83 @@ int run_chunks(irk_ctx *c, EnsArgs &a, char *ws, int64_t nblocks, int wpb, int s
         if ((rc = cuda_check(c, cudaGetLastError(), "advance_n launch"))) return rc;
     }
     return IRK_OK;
+}
+
+// ---- large-N single system (IRK_NBODY_DIRECT) ----
+int64_t nbd_nj(int64_t N) { return (N + irk::NBD_JBLOCK - 1) / irk::NBD_JBLOCK; }
+size_t nbd_bytes(const irk_ctx *c) {
+    if (c->problem != IRK_NBODY_DIRECT) return 0;
+    const size_t N = (size_t)c->dim / 6, d = 3 * N;
+    return 256 + sizeof(double) * (8 * d * 2 + 3 * d + (size_t)nbd_nj(N) * 8 * d);
+}
+
+int launch_direct(irk_ctx *c, double *y, double t0, char *ws, double *energy, int64_t *iters, cudaStream_t st) {
+    (void)t0;
+    const int64_t N = c->dim / 6, d = 3 * N;
+    int rc;
+    if (!c->d_mass) {
+        if ((rc = cuda_check(c, cudaMalloc(&c->d_mass, sizeof(double) * N), "cudaMalloc mass"))) return rc;
+        if ((rc = cuda_check(c, cudaMalloc(&c->d_rows, sizeof(double) * N), "cudaMalloc rows"))) return rc;
+        if ((rc = cuda_check(c, cudaMallocHost(&c->h_ctl, sizeof(irk::NbdCtl)), "cudaMallocHost ctl"))) return rc;
+    }
+    if ((rc = cuda_check(c, cudaMemcpyAsync(c->d_mass, c->params.data() + 2, sizeof(double) * N, cudaMemcpyHostToDevice, st),
+                         "H2D mass")))
+        return rc;
+    char *base = ws + kHeader + hist_bytes(c) + stats_bytes(c) + sched_bytes(c);
+    irk::NbdArgs a;
+    for (int j = 0; j < 8; ++j) a.hb[j] = c->T.hb[j];
+    a.y = y;
+    a.hist = reinterpret_cast<double *>(ws + kHeader);
+    a.ctl = reinterpret_cast<irk::NbdCtl *>(base);
+    a.Q = reinterpret_cast<double *>(base + 256);
+    a.V = a.Q + 8 * d;
+    a.M = a.V + 8 * d;
+    a.Pst = a.M + d;
+    a.sLq = a.Pst + d;
+    a.part = a.sLq + d;
+    a.mass = c->d_mass;
+    a.nbody = N;
+    a.nsteps = c->nsteps;
+    a.G = c->params[0];
+    a.eps2 = c->params[1] * c->params[1];
+    a.max_iters = c->max_iters;
+    int64_t *n_done = reinterpret_cast<int64_t *>(ws);
+    int64_t *stats = reinterpret_cast<int64_t *>(ws + kHeader + hist_bytes(c));
+    const unsigned cb = (unsigned)((d + 127) / 128);
+    const int64_t E = c->energy_every;
+    auto sample = [&](int64_t idx) {
+        irk::nbd_energy_rows_kernel<<<(unsigned)((N + 127) / 128), 128, 0, st>>>(y, c->d_mass, N, a.G, a.eps2, c->d_rows);
+        irk::nbd_energy_sum_kernel<<<1, 1, 0, st>>>(y, c->d_mass, N, c->d_rows, energy + idx);
+    };
+    if (E > 0 && energy) sample(0);
+    if ((rc = cuda_check(c, cudaMemsetAsync(a.ctl, 0, sizeof(irk::NbdCtl), st), "memset ctl"))) return rc;
+    // frozen (diverged earlier)?
+    int64_t bad0 = 0;
+    if ((rc = cuda_check(c, cudaMemcpyAsync(&bad0, stats + 1, sizeof(int64_t), cudaMemcpyDeviceToHost, st), "D2H bad")))
+        return rc;
+    if ((rc = cuda_check(c, cudaStreamSynchronize(st), "sync"))) return rc;
+    if (bad0 > 0 || c->nsteps == 0) {
+        if (iters) cudaMemsetAsync(iters, 0, sizeof(int64_t), st);
+        return cuda_check(c, cudaGetLastError(), "direct: frozen");
+    }
+    irk::nbd_init_kernel<<<cb, 128, 0, st>>>(a);
+    const dim3 fgrid((unsigned)((N + irk::NBD_FORCE_THREADS - 1) / irk::NBD_FORCE_THREADS), 8, (unsigned)nbd_nj(N));
+    int64_t n = 0;
+    while (n < c->nsteps) {
+        irk::nbd_pos_kernel<<<cb, 128, 0, st>>>(a);
+        irk::nbd_force_kernel<<<fgrid, irk::NBD_FORCE_THREADS, 0, st>>>(a);
+        irk::nbd_vel_kernel<<<cb, 128, 0, st>>>(a);
+        irk::nbd_ctl_kernel<<<1, 1, 0, st>>>(a, n_done, stats);
+        cudaMemcpyAsync(c->h_ctl, a.ctl, sizeof(irk::NbdCtl), cudaMemcpyDeviceToHost, st);
+        if ((rc = cuda_check(c, cudaStreamSynchronize(st), "direct sweep"))) return rc;
+        if (c->h_ctl->fin) {
+            n = c->h_ctl->n;
+            if (E > 0 && energy && n % E == 0) sample(n / E);
+            if (c->h_ctl->nonfinite) break;
+        }
+    }
+    if (iters) cudaMemcpyAsync(iters, &a.ctl->sweeps, sizeof(int64_t), cudaMemcpyDeviceToDevice, st);
+    return cuda_check(c, cudaGetLastError(), "direct launch");
 }
 
 EnsArgs ens_args(irk_ctx *c, double *y, double t0, char *ws, double *energy, int64_t *iters) {
@@ -313,7 +394,8 @@ irk_ctx *irk_create(int problem, int dim, double h, int64_t nsteps, int64_t batc
     }
     case IRK_NBODY_DIRECT:
         if (dim % 6 || dim < 12) return bad("irk_create: N-body needs dim = 6N, N >= 2");
-        return bad("irk_create: IRK_NBODY_DIRECT kernels not built yet");
+        if (batch != 1) return bad("irk_create: IRK_NBODY_DIRECT integrates one system (batch must be 1)");
+        break;
     default: return bad("irk_create: unknown problem");
     }
     if (!std::isfinite(h) || h == 0.0) return bad("irk_create: h must be finite and nonzero");
@@ -336,6 +418,8 @@ irk_ctx *irk_create(int problem, int dim, double h, int64_t nsteps, int64_t batc
 
 int irk_set_params(irk_ctx *c, const double *p, int n) {
     if (!c) return IRK_E_ARG;
+    if (c->problem == IRK_NBODY_DIRECT && p && n >= 2 && !(p[1] > 0.0))
+        return fail(c, IRK_E_ARG, "irk_set_params: IRK_NBODY_DIRECT needs eps > 0");
     if (!p || n != n_params_expected(c->problem, c->dim))
         return fail(c, IRK_E_ARG, "irk_set_params: expected %d params", n_params_expected(c->problem, c->dim));
     for (int i = 0; i < n; ++i)
@@ -374,7 +458,7 @@ int irk_set_option(irk_ctx *c, int key, int64_t val) {
 
 size_t irk_workspace_bytes(const irk_ctx *c) {
     if (!c) return 0;
-    return kHeader + hist_bytes(c) + stats_bytes(c) + sched_bytes(c);
+    return kHeader + hist_bytes(c) + stats_bytes(c) + sched_bytes(c) + nbd_bytes(c);
 }
 
 int irk_integrate(irk_ctx *c, double *y, double t0, void *workspace, double *energy, int64_t *iters,
@@ -404,6 +488,9 @@ int irk_integrate(irk_ctx *c, double *y, double t0, void *workspace, double *ene
         break;
     case IRK_FPU_BETA:
         rc = launch_chain(c, y, t0, ws, energy, iters, st);
+        break;
+    case IRK_NBODY_DIRECT:
+        rc = launch_direct(c, y, t0, ws, energy, iters, st);
         break;
     default: return fail(c, IRK_E_ARG, "irk_integrate: problem not supported");
     }
@@ -477,6 +564,20 @@ int irk_energy(irk_ctx *c, const double *y, double *H, void *stream) {
     case IRK_HENON_HEILES:
         energy_g1_kernel<<<blocks, threads, 0, st>>>(y, H, c->batch, irk::HenonHeiles{c->params[0], c->params[1]});
         break;
+    case IRK_NBODY_DIRECT: {
+        const int64_t N = c->dim / 6;
+        int rc;
+        if (!c->d_mass) {
+            if ((rc = cuda_check(c, cudaMalloc(&c->d_mass, sizeof(double) * N), "cudaMalloc mass"))) return rc;
+            if ((rc = cuda_check(c, cudaMalloc(&c->d_rows, sizeof(double) * N), "cudaMalloc rows"))) return rc;
+            if ((rc = cuda_check(c, cudaMallocHost(&c->h_ctl, sizeof(irk::NbdCtl)), "cudaMallocHost ctl"))) return rc;
+        }
+        cudaMemcpyAsync(c->d_mass, c->params.data() + 2, sizeof(double) * N, cudaMemcpyHostToDevice, st);
+        irk::nbd_energy_rows_kernel<<<(unsigned)((N + 127) / 128), 128, 0, st>>>(y, c->d_mass, N, c->params[0],
+                                                                                 c->params[1] * c->params[1], c->d_rows);
+        irk::nbd_energy_sum_kernel<<<1, 1, 0, st>>>(y, c->d_mass, N, c->d_rows, H);
+        break;
+    }
     case IRK_FPU_BETA: {
         const unsigned nb = (unsigned)((c->batch + 127) / 128);
         switch (c->dim / 2) {
@@ -562,6 +663,9 @@ void irk_destroy(irk_ctx *c) {
     cudaFree(c->d_energy);
     cudaFree(c->d_iters);
     cudaFree(c->d_ws);
+    cudaFree(c->d_mass);
+    cudaFree(c->d_rows);
+    if (c->h_ctl) cudaFreeHost(c->h_ctl);
     delete c;
 }
 

@@ -325,3 +325,29 @@ def test_fpu_other_sizes_and_energy_entry(irk, orc):
         H = ig.energy(torch.tensor(w.y, device="cuda")).cpu().numpy()
     Ho = np.array([orc.energy(w.problem, w.dim, w.params, w.y[:, b]) for b in range(w.batch)])
     assert np.array_equal(H, Ho)
+
+
+# ------------------------------------------------------------------ config 5
+def test_config5_plummer_small_full_length_energy(irk, orc):
+    """Plummer N = 1,024 (one j-block), 200 steps, energy every 50: the large-N
+    path (pos / blocked-force / vel kernels) vs the oracle, bitwise."""
+    w = wl.plummer(N=1024, nsteps=200)
+    g = run_gpu(irk, w, energy_every=50)
+    o = orc.integrate(w.problem, w.y, w.params, w.h, w.nsteps, energy_every=50)
+    assert_parity(g, o, energy=True)
+
+
+def test_config5_ragged_blocks(irk, orc):
+    """N = 2,500: three canonical j-blocks, the last one partial; 25 steps."""
+    w = wl.plummer(N=2500, nsteps=25)
+    g = run_gpu(irk, w, chunks=5)
+    o = orc.integrate(w.problem, w.y, w.params, w.h, w.nsteps)
+    assert_parity(g, o)
+
+
+def test_config5_full_size_first_steps(irk, orc):
+    """Config 5 at full size (N = 8,192) for the first 4 steps, bitwise."""
+    w = wl.plummer(nsteps=4)
+    g = run_gpu(irk, w, energy_every=2)
+    o = orc.integrate(w.problem, w.y, w.params, w.h, w.nsteps, energy_every=2)
+    assert_parity(g, o, energy=True)
