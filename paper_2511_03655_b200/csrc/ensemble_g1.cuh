@@ -249,3 +249,126 @@ __global__ void __maxnreg__(G1_MAXREG) ens_g1_kernel(const __grid_constant__ Ens
 }
 
 }  // namespace irk
+
+namespace irk {
+
+// First-order mode (Eqs. IRK_init / IRK_FP) for the per-thread
+// problems: all D = 2d components are extrapolated (a1 over y), each sweep
+// evaluates F_i = (V-part of Y_i, g(Q-part of Y_i, t_i)), L = hb o F,
+// Y_i = y + D(mu_i, L), and the stop test runs over all D components from k = 1
+// (Delta^[1] = |Y^[1] - Y^[0]| exists here).  Reading R-6 of DESIGN.md: this form
+// can false-stop on second-order systems (SURVEY C-6), so partitioned mode is the
+// default; this kernel serves IRK_OPT_MODE = 1.  One thread per trajectory,
+// per-step loop (not performance-tuned).
+template <class P>
+__global__ void __launch_bounds__(64) ens_g1fo_kernel(const __grid_constant__ EnsArgs a,
+                                                      const __grid_constant__ P prob) {
+    constexpr int d = P::d, D = 2 * d;
+    const int64_t B = a.batch;
+    const int64_t slot = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (slot >= a.nslots) return;
+    const int64_t b = a.perm ? (int64_t)a.perm[slot] : slot;
+    if (b < 0 || b >= B) return;
+    double y[D];
+#pragma unroll
+    for (int l = 0; l < D; ++l) y[l] = a.y[l * B + b];
+    int64_t bad = a.stats[1 * B + b];
+    const int64_t n0 = *a.n_done;
+    const bool sample = (a.energy != nullptr) && (a.energy_every > 0);
+    if (sample && a.c0 == 0) a.energy[b] = prob.energy(y, y + d);
+    if (bad > 0 || a.nsteps == 0) {
+        if (a.iters && a.c0 == 0) a.iters[b] = 0;
+        if (a.csweeps) a.csweeps[b] = 0;
+        return;
+    }
+    double L[8][D];
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+#pragma unroll
+        for (int l = 0; l < D; ++l) L[j][l] = a.hist[((int64_t)j * D + l) * B + b];
+    const double kInf = __longlong_as_double(0x7ff0000000000000LL);
+    int64_t hits = 0, sweeps = 0, n = 0;
+    for (; n < a.nsteps;) {
+        double Y[8][D], m[D], p[D];
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+#pragma unroll
+            for (int l = 0; l < D; ++l) {
+                double acc = dmul(c_nu[i][0], L[0][l]);
+#pragma unroll
+                for (int j = 1; j < 8; ++j) acc = dfma(c_nu[i][j], L[j][l], acc);
+                Y[i][l] = dadd(y[l], acc);
+            }
+#pragma unroll
+        for (int l = 0; l < D; ++l) m[l] = p[l] = kInf;
+        const double tn1 = dadd(a.t0, dmul((double)(n0 + n), a.h));
+        int k = 0;
+        bool stop = false;
+        for (;;) {
+            ++k;
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                double F[d];
+                bool ok = true;
+                prob.template accel<true>(Y[i], F, dadd(tn1, dmul(c_c[i], a.h)), ok);
+#pragma unroll
+                for (int l = 0; l < d; ++l) {
+                    L[i][l] = dmul(a.hb[i], Y[i][d + l]);
+                    L[i][d + l] = dmul(a.hb[i], F[l]);
+                }
+            }
+            stop = true;
+#pragma unroll
+            for (int l = 0; l < D; ++l) {
+                double delta = 0.0;
+#pragma unroll
+                for (int i = 0; i < 8; ++i) {
+                    double acc = dmul(c_mu[i][0], L[0][l]);
+#pragma unroll
+                    for (int j = 1; j < 8; ++j) acc = dfma(c_mu[i][j], L[j][l], acc);
+                    const double yn = dadd(y[l], acc);
+                    const double e = dabs(dsub(yn, Y[i][l]));
+                    delta = (e > delta) ? e : delta;
+                    Y[i][l] = yn;
+                }
+                const double mn = (delta < p[l]) ? delta : p[l];
+                const bool okc = (delta == 0.0) || (m[l] <= mn);
+                m[l] = (p[l] < m[l]) ? p[l] : m[l];
+                p[l] = delta;
+                stop = stop && okc;
+            }
+            if (stop || k >= a.max_iters) break;
+        }
+        bool finite = true;
+#pragma unroll
+        for (int l = 0; l < D; ++l) {
+            double s = L[0][l];
+#pragma unroll
+            for (int j = 1; j < 8; ++j) s = dadd(s, L[j][l]);
+            y[l] = dadd(y[l], s);
+            finite = finite && isfinite(y[l]);
+        }
+        ++n;
+        sweeps += k;
+        hits += stop ? 0 : 1;
+        if (sample && ((a.c0 + n) % a.energy_every) == 0)
+            a.energy[((a.c0 + n) / a.energy_every) * B + b] = prob.energy(y, y + d);
+        if (!finite) {
+            bad = n0 + n;
+            break;
+        }
+    }
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+#pragma unroll
+        for (int l = 0; l < D; ++l) a.hist[((int64_t)j * D + l) * B + b] = L[j][l];
+#pragma unroll
+    for (int l = 0; l < D; ++l) a.y[l * B + b] = y[l];
+    a.stats[0 * B + b] += hits;
+    a.stats[1 * B + b] = bad;
+    a.stats[2 * B + b] += sweeps;
+    if (a.iters) a.iters[b] = (a.c0 == 0) ? sweeps : a.iters[b] + sweeps;
+    if (a.csweeps) a.csweeps[b] = (int32_t)sweeps;
+}
+
+}  // namespace irk

@@ -272,6 +272,10 @@ int launch_g1(irk_ctx *c, const P &prob, double *y, double t0, char *ws, double 
               int64_t *iters, cudaStream_t st) {
     EnsArgs a = ens_args(c, y, t0, ws, energy, iters);
     const int64_t blocks = (c->batch + irk::G1_THREADS - 1) / irk::G1_THREADS;
+    if (c->mode == 1)
+        return run_chunks(c, a, ws, blocks, irk::G1_THREADS / 32, 32, st, [&](const EnsArgs &aa, int64_t nb) {
+            irk::ens_g1fo_kernel<P><<<(unsigned)nb, irk::G1_THREADS, 0, st>>>(aa, prob);
+        });
     return run_chunks(c, a, ws, blocks, irk::G1_THREADS / 32, 32, st, [&](const EnsArgs &aa, int64_t nb) {
         irk::ens_g1_kernel<P><<<(unsigned)nb, irk::G1_THREADS, 0, st>>>(aa, prob);
     });
@@ -433,7 +437,9 @@ int irk_set_option(irk_ctx *c, int key, int64_t val) {
     if (!c) return IRK_E_ARG;
     switch (key) {
     case IRK_OPT_MODE:
-        if (val != 0) return fail(c, IRK_E_ARG, "irk_set_option: first-order mode not built yet");
+        if (val != 0 && val != 1) return fail(c, IRK_E_ARG, "irk_set_option: MODE must be 0 or 1");
+        if (val == 1 && c->problem != IRK_KEPLER && c->problem != IRK_HENON_HEILES)
+            return fail(c, IRK_E_ARG, "irk_set_option: first-order mode is built for Kepler and Henon-Heiles");
         c->mode = (int)val;
         return IRK_OK;
     case IRK_OPT_MAX_ITERS:

@@ -351,3 +351,25 @@ def test_config5_full_size_first_steps(irk, orc):
     g = run_gpu(irk, w, energy_every=2)
     o = orc.integrate(w.problem, w.y, w.params, w.h, w.nsteps, energy_every=2)
     assert_parity(g, o, energy=True)
+
+
+# ---------------------------------------------------------- first-order mode
+def test_first_order_mode_parity(irk, orc):
+    """IRK_OPT_MODE = 1 (Eqs. IRK_init / IRK_FP, stop test over all D from k = 1)
+    vs the oracle's first-order step, bitwise, Kepler and Henon-Heiles, chunked."""
+    for w in (wl.kepler_ensemble(batch=200, nsteps=600), wl.henon_heiles(batch=70, nsteps=600, h=0.05)):
+        with irk.Integrator(w.problem, w.dim, w.h, 200, w.batch, w.params, mode=irk.FIRST_ORDER,
+                            energy_every=100) as ig:
+            Y = torch.tensor(w.y, dtype=torch.float64, device="cuda")
+            ws = ig.new_workspace()
+            it = torch.zeros(w.batch, dtype=torch.int64, device="cuda")
+            E = torch.zeros((ig.n_energy(), w.batch), dtype=torch.float64, device="cuda")
+            tot = np.zeros(w.batch, dtype=np.int64)
+            for _ in range(3):
+                ig.integrate(Y, ws, energy=E, iters=it)
+                tot += it.cpu().numpy()
+            y = Y.cpu().numpy()
+            hist = ig.hist_view(ws).cpu().numpy()
+        o = orc.integrate(w.problem, w.y, w.params, w.h, 600, mode=orc.FIRST_ORDER)
+        assert np.array_equal(y, o["y"]) and np.array_equal(tot, o["iters"])
+        assert np.array_equal(hist, o["hist"].transpose(1, 2, 0))

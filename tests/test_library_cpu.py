@@ -79,6 +79,9 @@ def test_params_and_options_errors(irk):
         irk.Integrator(irk.KEPLER, 4, 0.1, 10, 4, params=[float("inf")])
     with pytest.raises(irk.IrkError):
         irk.Integrator(irk.KEPLER, 4, 0.1, 10, 4, params=[1.0], max_iters=0)
+    with pytest.raises(irk.IrkError):  # first-order mode is built for the per-thread problems only
+        irk.Integrator(irk.FPU_BETA, 128, 0.1, 10, 4, params=[1.0], mode=irk.FIRST_ORDER)
+    irk.Integrator(irk.HENON_HEILES, 4, 0.1, 10, 4, params=[1.0, 0.0], mode=irk.FIRST_ORDER).close()
     w = irk.Integrator(irk.KEPLER, 4, -0.1, 10, 4, params=[1.0])  # negative h is allowed
     assert w.workspace_bytes == 64 + 8 * 8 * 4 * 4 + 8 * 4 * 4 + 4 * (64 + 2 * 4 + 1024)
     w.close()

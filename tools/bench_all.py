@@ -32,6 +32,9 @@ def f_flops(w):
     if w.problem == wl.NBODY:
         N = w.dim // 6
         return 26 * N * (N - 1) // 2
+    if w.problem == wl.NBODY_DIRECT:  # canonical direct sum incl. j = i: 19 flops per (i, j)
+        N = w.dim // 6
+        return 19 * N * N
     raise ValueError
 
 
@@ -68,7 +71,7 @@ def run(cfg, reps):
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--configs", default="1,2,3,4")
+    ap.add_argument("--configs", default="1,2,3,4,5")
     ap.add_argument("--reps", type=int, default=2)
     ap.add_argument("--out", default="")
     a = ap.parse_args()
