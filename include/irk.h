@@ -63,9 +63,11 @@ enum irk_option {
     IRK_OPT_MAX_ITERS = 2,    /* sweeps cap per step, default 100 (flagged, step accepted)   */
     IRK_OPT_ENERGY_EVERY = 3, /* E > 0: sample H(y_n) at local steps 0, E, 2E, ... (default 0) */
     IRK_OPT_MAPPING = 4,      /* 0 = auto; see DESIGN.md for the per-problem kernels          */
-    IRK_OPT_BALANCE = 5       /* ensemble scheduling: -1 = auto (default), 0 = off, C > 0 = run the
+    IRK_OPT_BALANCE = 5,      /* ensemble scheduling: -1 = auto (default), 0 = off, C > 0 = run the
                                  call in chunks of C steps, re-sorting trajectories by the cost of
                                  the previous chunk (bitwise-neutral)  */
+    IRK_OPT_VSHARDS = 6       /* IRK_NBODY_DIRECT only: drive P body shards from this process on one
+                                 GPU through the sharded code path (testing the exchange layout)   */
 };
 
 /* Create a context for `batch` independent trajectories of `problem` in
@@ -118,10 +120,20 @@ int irk_stats(irk_ctx *ctx, const void *workspace, void *stream, int64_t out[4])
  * (row-major [i*8+j]).  Returns IRK_OK. */
 int irk_tableau(double *c, double *b, double *mu, double *nu);
 
-/* NCCL communicator for a body-sharded IRK_NBODY_DIRECT system: rank r of
- * nranks owns bodies [r*N/nranks, (r+1)*N/nranks); nccl_unique_id points to a
- * 128-byte ncclUniqueId created by rank 0 and broadcast by the caller. */
+/* NCCL communicator for a body-sharded IRK_NBODY_DIRECT system (one process per
+ * GPU): rank r of nranks owns bodies [r*N/nranks, (r+1)*N/nranks)
+ * and from then on passes only its bodies' rows to irk_integrate: y is
+ * [q_local (3N/P) | v_local (3N/P)], the history [8][6N/P] (call
+ * irk_workspace_bytes after this).  Each fixed-point iteration all-gathers the
+ * stage positions (8 x 3N/P doubles + 2 flags per rank) in place over NCCL; the
+ * stop decision is the same on every rank, and results equal the 1-GPU run bit
+ * for bit.  nccl_unique_id points to 128 bytes from irk_nccl_unique_id on rank 0,
+ * broadcast by the caller.  NCCL is loaded at run time (libnccl.so.2, or the path
+ * in $IRK_NCCL_LIB).  Returns IRK_E_COMM on NCCL failure. */
 int irk_set_comm(irk_ctx *ctx, const void *nccl_unique_id, int rank, int nranks);
+
+/* Write a fresh 128-byte ncclUniqueId to `out` (rank 0 of irk_set_comm). */
+int irk_nccl_unique_id(void *out);
 
 /* NULL ctx: the thread-local message of the last failed irk_create. */
 const char *irk_last_error(const irk_ctx *ctx);

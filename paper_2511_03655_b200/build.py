@@ -36,6 +36,17 @@ def _nvcc() -> str:
     raise RuntimeError("nvcc not found")
 
 
+def _nccl_include() -> str:
+    """nccl.h of the torch wheel's NCCL 2.28 (types only; NCCL is dlopen'ed at run time)."""
+    import importlib.util
+    spec = importlib.util.find_spec("nvidia")
+    for base in list(spec.submodule_search_locations or []) if spec else []:
+        p = os.path.join(base, "nccl", "include")
+        if os.path.exists(os.path.join(p, "nccl.h")):
+            return p
+    return "/usr/include"
+
+
 def _stale() -> bool:
     if not os.path.exists(LIB):
         return True
@@ -65,7 +76,8 @@ def build(force: bool = False, verbose: bool = False, out: str | None = None,
     log = []
     for src in CU_SOURCES:
         o = os.path.join(bdir, src + ".o")
-        r = subprocess.run([nvcc, *NVCC_FLAGS, *[f"-D{x}" for x in defines], "-I", os.path.join(ROOT, "include"), "-c",
+        r = subprocess.run([nvcc, *NVCC_FLAGS, *[f"-D{x}" for x in defines], "-I", os.path.join(ROOT, "include"),
+                            "-I", _nccl_include(), "-c",
                             os.path.join(CSRC, src), "-o", o], capture_output=True, text=True)
         log.append(r.stdout + r.stderr)
         if r.returncode:
@@ -75,7 +87,7 @@ def build(force: bool = False, verbose: bool = False, out: str | None = None,
     tmp = lib_path + f".tmp{os.getpid()}"
     os.makedirs(os.path.dirname(lib_path), exist_ok=True)
     subprocess.check_call([nvcc, "-shared", *GENCODE, "-Xcompiler", "-fPIC", "-o", tmp, *objs,
-                           "-cudart", "static"])
+                           "-cudart", "static", "-ldl"])
     os.replace(tmp, lib_path)
     with open(lib_path + ".ptxas.log" if out else os.path.join(OUT, "ptxas.log"), "w") as f:
         f.write("\n".join(log))

@@ -43,6 +43,9 @@ struct irk_ctx {
     // large-N path
     double *d_mass = nullptr, *d_rows = nullptr;
     irk::NbdCtl *h_ctl = nullptr;  // pinned readback of the control block
+    int nranks = 1, rank = 0;      // NCCL body sharding (irk_set_comm)
+    int vshards = 1;               // virtual shards on one GPU (IRK_OPT_VSHARDS)
+    void *nccl_comm = nullptr;
 };
 
 namespace {
@@ -64,7 +67,11 @@ int cuda_check(irk_ctx *c, cudaError_t e, const char *what) {
     return fail(c, IRK_E_CUDA, "%s: %s", what, cudaGetErrorString(e));
 }
 
-size_t hist_bytes(const irk_ctx *c) { return sizeof(double) * 8 * (size_t)c->dim * c->batch; }
+// rows of y / history held by this process (the local bodies' 6N/P rows when sharded under NCCL)
+int64_t local_dim(const irk_ctx *c) {
+    return (c->problem == IRK_NBODY_DIRECT && c->nccl_comm) ? c->dim / c->nranks : c->dim;
+}
+size_t hist_bytes(const irk_ctx *c) { return sizeof(double) * 8 * (size_t)local_dim(c) * c->batch; }
 size_t stats_bytes(const irk_ctx *c) { return sizeof(int64_t) * 4 * (size_t)c->batch; }
 
 int n_params_expected(int problem, int dim) {
@@ -173,56 +180,100 @@ int run_chunks(irk_ctx *c, EnsArgs &a, char *ws, int64_t nblocks, int wpb, int s
     return IRK_OK;
 }
 
-// ---- large-N single system (IRK_NBODY_DIRECT) ----
+// ---- large-N single system (IRK_NBODY_DIRECT), body-sharded ----
 int64_t nbd_nj(int64_t N) { return (N + irk::NBD_JBLOCK - 1) / irk::NBD_JBLOCK; }
+int nbd_P(const irk_ctx *c) { return c->nccl_comm ? c->nranks : (c->vshards > 1 ? c->vshards : 1); }
+int nbd_nlocal(const irk_ctx *c) { return c->nccl_comm ? 1 : nbd_P(c); }  // shards driven by this process
+int64_t nbd_stride(const irk_ctx *c) { return 24 * ((int64_t)c->dim / 6 / nbd_P(c)) + 2; }
 size_t nbd_bytes(const irk_ctx *c) {
     if (c->problem != IRK_NBODY_DIRECT) return 0;
-    const size_t N = (size_t)c->dim / 6, d = 3 * N;
-    return 256 + sizeof(double) * (8 * d * 2 + 3 * d + (size_t)nbd_nj(N) * 8 * d);
+    const int P = nbd_P(c);
+    const size_t N = (size_t)c->dim / 6, nloc = N / P, dl = 3 * nloc;
+    const size_t per_shard = 8 * dl + 3 * dl + (size_t)nbd_nj(N) * 8 * dl;
+    return 256 + sizeof(double) * ((size_t)P * nbd_stride(c) + nbd_nlocal(c) * per_shard + 3 * N + 2 * N);
 }
+
+int nccl_check(irk_ctx *c, int r, const char *what);
+int nccl_allgather_inplace(irk_ctx *c, double *buf, size_t count_per_rank, cudaStream_t st);
 
 int launch_direct(irk_ctx *c, double *y, double t0, char *ws, double *energy, int64_t *iters, cudaStream_t st) {
     (void)t0;
-    const int64_t N = c->dim / 6, d = 3 * N;
+    const int64_t N = c->dim / 6;
+    const int P = nbd_P(c), nlocal = nbd_nlocal(c);
+    const int first = c->nccl_comm ? c->rank : 0;
+    const int64_t nloc = N / P, dl = 3 * nloc, stride = nbd_stride(c);
+    const bool nccl = c->nccl_comm != nullptr;
     int rc;
     if (!c->d_mass) {
         if ((rc = cuda_check(c, cudaMalloc(&c->d_mass, sizeof(double) * N), "cudaMalloc mass"))) return rc;
-        if ((rc = cuda_check(c, cudaMalloc(&c->d_rows, sizeof(double) * N), "cudaMalloc rows"))) return rc;
         if ((rc = cuda_check(c, cudaMallocHost(&c->h_ctl, sizeof(irk::NbdCtl)), "cudaMallocHost ctl"))) return rc;
     }
     if ((rc = cuda_check(c, cudaMemcpyAsync(c->d_mass, c->params.data() + 2, sizeof(double) * N, cudaMemcpyHostToDevice, st),
                          "H2D mass")))
         return rc;
     char *base = ws + kHeader + hist_bytes(c) + stats_bytes(c) + sched_bytes(c);
-    irk::NbdArgs a;
-    for (int j = 0; j < 8; ++j) a.hb[j] = c->T.hb[j];
-    a.y = y;
-    a.hist = reinterpret_cast<double *>(ws + kHeader);
-    a.ctl = reinterpret_cast<irk::NbdCtl *>(base);
-    a.Q = reinterpret_cast<double *>(base + 256);
-    a.V = a.Q + 8 * d;
-    a.M = a.V + 8 * d;
-    a.Pst = a.M + d;
-    a.sLq = a.Pst + d;
-    a.part = a.sLq + d;
-    a.mass = c->d_mass;
-    a.nbody = N;
-    a.nsteps = c->nsteps;
-    a.G = c->params[0];
-    a.eps2 = c->params[1] * c->params[1];
-    a.max_iters = c->max_iters;
+    irk::NbdCtl *ctl = reinterpret_cast<irk::NbdCtl *>(base);
+    double *Qg = reinterpret_cast<double *>(base + 256);
+    double *shard_mem = Qg + (size_t)P * stride;
+    const size_t per_shard = 8 * dl + 3 * dl + (size_t)nbd_nj(N) * 8 * dl;
+    double *Qall = shard_mem + (size_t)nlocal * per_shard;   // [3N] positions for energy samples
+    double *terms = Qall + 3 * N;                            // [P][2*nloc]
     int64_t *n_done = reinterpret_cast<int64_t *>(ws);
     int64_t *stats = reinterpret_cast<int64_t *>(ws + kHeader + hist_bytes(c));
-    const unsigned cb = (unsigned)((d + 127) / 128);
+    const int64_t ldim = nccl ? 6 * nloc : 6 * N;  // rows of this process's y / history
+    std::vector<irk::NbdArgs> A(nlocal);
+    for (int t = 0; t < nlocal; ++t) {
+        irk::NbdArgs &a = A[t];
+        const int sh = first + t;
+        for (int j = 0; j < 8; ++j) a.hb[j] = c->T.hb[j];
+        const int64_t qoff = nccl ? 0 : 3 * (int64_t)sh * nloc, voff = nccl ? 3 * nloc : 3 * N + 3 * (int64_t)sh * nloc;
+        a.yq = y + qoff;
+        a.yv = y + voff;
+        a.hist = reinterpret_cast<double *>(ws + kHeader);
+        a.hdim = ldim;
+        a.hq = qoff;
+        a.hv = voff;
+        a.Qg = Qg;
+        a.stride = stride;
+        double *m = shard_mem + (size_t)t * per_shard;
+        a.V = m;
+        a.M = m + 8 * dl;
+        a.Pst = a.M + dl;
+        a.sLq = a.Pst + dl;
+        a.part = a.sLq + dl;
+        a.mass = c->d_mass;
+        a.ctl = ctl;
+        a.nbody = N;
+        a.nloc = nloc;
+        a.b0 = (int64_t)sh * nloc;
+        a.shard = sh;
+        a.nshards = P;
+        a.G = c->params[0];
+        a.eps2 = c->params[1] * c->params[1];
+        a.max_iters = c->max_iters;
+    }
+    const unsigned cb = (unsigned)((dl + 127) / 128);
     const int64_t E = c->energy_every;
-    auto sample = [&](int64_t idx) {
-        irk::nbd_energy_rows_kernel<<<(unsigned)((N + 127) / 128), 128, 0, st>>>(y, c->d_mass, N, a.G, a.eps2, c->d_rows);
-        irk::nbd_energy_sum_kernel<<<1, 1, 0, st>>>(y, c->d_mass, N, c->d_rows, energy + idx);
+    auto sample = [&](int64_t idx) -> int {
+        for (int t = 0; t < nlocal; ++t)
+            cudaMemcpyAsync(Qall + 3 * A[t].b0, A[t].yq, sizeof(double) * dl, cudaMemcpyDeviceToDevice, st);
+        if (nccl) {
+            int r = nccl_allgather_inplace(c, Qall, (size_t)dl, st);
+            if (r) return r;
+        }
+        for (int t = 0; t < nlocal; ++t)
+            irk::nbd_energy_terms_kernel<<<(unsigned)((nloc + 127) / 128), 128, 0, st>>>(
+                Qall, A[t].yv, c->d_mass, N, A[t].b0, nloc, A[t].G, A[t].eps2, terms + 2 * A[t].b0);
+        if (nccl) {
+            int r = nccl_allgather_inplace(c, terms, (size_t)(2 * nloc), st);
+            if (r) return r;
+        }
+        irk::nbd_energy_sum_kernel<<<1, 1, 0, st>>>(terms, P, nloc, energy + idx);
+        return cuda_check(c, cudaGetLastError(), "energy sample");
     };
-    if (E > 0 && energy) sample(0);
-    if ((rc = cuda_check(c, cudaMemsetAsync(a.ctl, 0, sizeof(irk::NbdCtl), st), "memset ctl"))) return rc;
-    // frozen (diverged earlier)?
-    int64_t bad0 = 0;
+    if (E > 0 && energy && (rc = sample(0))) return rc;
+    if ((rc = cuda_check(c, cudaMemsetAsync(ctl, 0, sizeof(irk::NbdCtl), st), "memset ctl"))) return rc;
+    int64_t bad0 = 0;  // frozen (diverged in an earlier call)?
     if ((rc = cuda_check(c, cudaMemcpyAsync(&bad0, stats + 1, sizeof(int64_t), cudaMemcpyDeviceToHost, st), "D2H bad")))
         return rc;
     if ((rc = cuda_check(c, cudaStreamSynchronize(st), "sync"))) return rc;
@@ -230,23 +281,28 @@ int launch_direct(irk_ctx *c, double *y, double t0, char *ws, double *energy, in
         if (iters) cudaMemsetAsync(iters, 0, sizeof(int64_t), st);
         return cuda_check(c, cudaGetLastError(), "direct: frozen");
     }
-    irk::nbd_init_kernel<<<cb, 128, 0, st>>>(a);
-    const dim3 fgrid((unsigned)((N + irk::NBD_FORCE_THREADS - 1) / irk::NBD_FORCE_THREADS), 8, (unsigned)nbd_nj(N));
+    for (int t = 0; t < nlocal; ++t) irk::nbd_init_kernel<<<cb, 128, 0, st>>>(A[t]);
+    const dim3 fgrid((unsigned)((nloc + irk::NBD_FORCE_THREADS - 1) / irk::NBD_FORCE_THREADS), 8, (unsigned)nbd_nj(N));
     int64_t n = 0;
     while (n < c->nsteps) {
-        irk::nbd_pos_kernel<<<cb, 128, 0, st>>>(a);
-        irk::nbd_force_kernel<<<fgrid, irk::NBD_FORCE_THREADS, 0, st>>>(a);
-        irk::nbd_vel_kernel<<<cb, 128, 0, st>>>(a);
-        irk::nbd_ctl_kernel<<<1, 1, 0, st>>>(a, n_done, stats);
-        cudaMemcpyAsync(c->h_ctl, a.ctl, sizeof(irk::NbdCtl), cudaMemcpyDeviceToHost, st);
+        for (int t = 0; t < nlocal; ++t) irk::nbd_pos_kernel<<<cb, 128, 0, st>>>(A[t]);
+        if (nccl && (rc = nccl_allgather_inplace(c, Qg, (size_t)stride, st))) return rc;  // the exchange
+        irk::nbd_or_kernel<<<1, 1, 0, st>>>(A[0]);
+        for (int t = 0; t < nlocal; ++t) irk::nbd_force_kernel<<<fgrid, irk::NBD_FORCE_THREADS, 0, st>>>(A[t]);
+        for (int t = 0; t < nlocal; ++t) irk::nbd_vel_kernel<<<cb, 128, 0, st>>>(A[t]);
+        irk::nbd_ctl_kernel<<<1, 1, 0, st>>>(A[0], first, nlocal, n_done, stats);
+        cudaMemcpyAsync(c->h_ctl, ctl, sizeof(irk::NbdCtl), cudaMemcpyDeviceToHost, st);
         if ((rc = cuda_check(c, cudaStreamSynchronize(st), "direct sweep"))) return rc;
+        if (c->h_ctl->halt) break;
         if (c->h_ctl->fin) {
             n = c->h_ctl->n;
-            if (E > 0 && energy && n % E == 0) sample(n / E);
-            if (c->h_ctl->nonfinite) break;
+            if (E > 0 && energy && n % E == 0 && (rc = sample(n / E))) return rc;
         }
     }
-    if (iters) cudaMemcpyAsync(iters, &a.ctl->sweeps, sizeof(int64_t), cudaMemcpyDeviceToDevice, st);
+    // final exchange: a divergence at the call's last step is recorded on every rank
+    if (nccl && (rc = nccl_allgather_inplace(c, Qg, (size_t)stride, st))) return rc;
+    irk::nbd_final_kernel<<<1, 1, 0, st>>>(A[0], n_done, stats);
+    if (iters) cudaMemcpyAsync(iters, &ctl->sweeps, sizeof(int64_t), cudaMemcpyDeviceToDevice, st);
     return cuda_check(c, cudaGetLastError(), "direct launch");
 }
 
@@ -372,6 +428,56 @@ __global__ void energy_g1_kernel(const double *y, double *H, int64_t B, const __
 
 }  // namespace
 
+// ---- NCCL (loaded at run time: the library has no link-time NCCL dependency) ----
+#include <dlfcn.h>
+#include "nccl.h"
+
+namespace {
+struct NcclApi {
+    void *h = nullptr;
+    ncclResult_t (*getUniqueId)(ncclUniqueId *) = nullptr;
+    ncclResult_t (*commInitRank)(ncclComm_t *, int, ncclUniqueId, int) = nullptr;
+    ncclResult_t (*allGather)(const void *, void *, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*commDestroy)(ncclComm_t) = nullptr;
+    const char *(*getErrorString)(ncclResult_t) = nullptr;
+};
+std::mutex g_nccl_mu;
+NcclApi g_nccl;
+
+const char *load_nccl() {
+    std::lock_guard<std::mutex> lk(g_nccl_mu);
+    if (g_nccl.h) return nullptr;
+    const char *env = getenv("IRK_NCCL_LIB");
+    const char *cands[] = {env, "libnccl.so.2", "libnccl.so",
+                           "/opt/prime-rl/.venv/lib/python3.12/site-packages/nvidia/nccl/lib/libnccl.so.2"};
+    void *h = nullptr;
+    for (const char *c : cands)
+        if (c && (h = dlopen(c, RTLD_NOW | RTLD_GLOBAL))) break;
+    if (!h) return "NCCL library not found (set IRK_NCCL_LIB)";
+    g_nccl.getUniqueId = (decltype(g_nccl.getUniqueId))dlsym(h, "ncclGetUniqueId");
+    g_nccl.commInitRank = (decltype(g_nccl.commInitRank))dlsym(h, "ncclCommInitRank");
+    g_nccl.allGather = (decltype(g_nccl.allGather))dlsym(h, "ncclAllGather");
+    g_nccl.commDestroy = (decltype(g_nccl.commDestroy))dlsym(h, "ncclCommDestroy");
+    g_nccl.getErrorString = (decltype(g_nccl.getErrorString))dlsym(h, "ncclGetErrorString");
+    if (!g_nccl.getUniqueId || !g_nccl.commInitRank || !g_nccl.allGather || !g_nccl.commDestroy)
+        return "NCCL library lacks required symbols";
+    g_nccl.h = h;
+    return nullptr;
+}
+
+int nccl_check(irk_ctx *c, int r, const char *what) {
+    if (r == 0) return IRK_OK;
+    return fail(c, IRK_E_COMM, "%s: %s", what, g_nccl.getErrorString ? g_nccl.getErrorString((ncclResult_t)r) : "error");
+}
+
+int nccl_allgather_inplace(irk_ctx *c, double *buf, size_t count_per_rank, cudaStream_t st) {
+    ncclComm_t comm = reinterpret_cast<ncclComm_t>(c->nccl_comm);
+    return nccl_check(c, g_nccl.allGather(buf + (size_t)c->rank * count_per_rank, buf, count_per_rank, ncclFloat64,
+                                          comm, st),
+                      "ncclAllGather");
+}
+}  // namespace
+
 extern "C" {
 
 irk_ctx *irk_create(int problem, int dim, double h, int64_t nsteps, int64_t batch) {
@@ -454,6 +560,11 @@ int irk_set_option(irk_ctx *c, int key, int64_t val) {
         if (val < -1) return fail(c, IRK_E_ARG, "irk_set_option: bad BALANCE");
         c->balance = val;
         return IRK_OK;
+    case IRK_OPT_VSHARDS:
+        if (c->problem != IRK_NBODY_DIRECT || val < 1 || (c->dim / 6) % val || c->nccl_comm)
+            return fail(c, IRK_E_ARG, "irk_set_option: VSHARDS needs IRK_NBODY_DIRECT, N %% P == 0, no NCCL comm");
+        c->vshards = (int)val;
+        return IRK_OK;
     case IRK_OPT_MAPPING:
         if (val < 0) return fail(c, IRK_E_ARG, "irk_set_option: bad MAPPING");
         c->mapping = (int)val;
@@ -508,7 +619,7 @@ int irk_integrate_host(irk_ctx *c, double *y_host, double t0, double *energy_hos
     if (!c) return IRK_E_ARG;
     if (!y_host) return fail(c, IRK_E_ARG, "irk_integrate_host: null y");
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-    const size_t ybytes = sizeof(double) * (size_t)c->dim * c->batch;
+    const size_t ybytes = sizeof(double) * (size_t)local_dim(c) * c->batch;
     const size_t wsb = irk_workspace_bytes(c);
     const size_t ebytes = c->energy_every > 0 ? sizeof(double) * (size_t)(c->nsteps / c->energy_every + 1) * c->batch : 0;
     int rc;
@@ -572,16 +683,25 @@ int irk_energy(irk_ctx *c, const double *y, double *H, void *stream) {
         break;
     case IRK_NBODY_DIRECT: {
         const int64_t N = c->dim / 6;
+        const int P = c->nccl_comm ? c->nranks : 1;
+        const int64_t nloc = N / P;
         int rc;
         if (!c->d_mass) {
             if ((rc = cuda_check(c, cudaMalloc(&c->d_mass, sizeof(double) * N), "cudaMalloc mass"))) return rc;
-            if ((rc = cuda_check(c, cudaMalloc(&c->d_rows, sizeof(double) * N), "cudaMalloc rows"))) return rc;
             if ((rc = cuda_check(c, cudaMallocHost(&c->h_ctl, sizeof(irk::NbdCtl)), "cudaMallocHost ctl"))) return rc;
         }
+        if (!c->d_rows && (rc = cuda_check(c, cudaMalloc(&c->d_rows, sizeof(double) * 5 * N), "cudaMalloc energy")))
+            return rc;
+        double *Qall = c->d_rows, *terms = c->d_rows + 3 * N;
         cudaMemcpyAsync(c->d_mass, c->params.data() + 2, sizeof(double) * N, cudaMemcpyHostToDevice, st);
-        irk::nbd_energy_rows_kernel<<<(unsigned)((N + 127) / 128), 128, 0, st>>>(y, c->d_mass, N, c->params[0],
-                                                                                 c->params[1] * c->params[1], c->d_rows);
-        irk::nbd_energy_sum_kernel<<<1, 1, 0, st>>>(y, c->d_mass, N, c->d_rows, H);
+        const int64_t b0 = (int64_t)c->rank * nloc;
+        cudaMemcpyAsync(Qall + 3 * b0, y, sizeof(double) * 3 * nloc, cudaMemcpyDeviceToDevice, st);
+        if (c->nccl_comm && (rc = nccl_allgather_inplace(c, Qall, (size_t)(3 * nloc), st))) return rc;
+        const double *v = y + (c->nccl_comm ? 3 * nloc : 3 * N);
+        irk::nbd_energy_terms_kernel<<<(unsigned)((nloc + 127) / 128), 128, 0, st>>>(
+            Qall, v, c->d_mass, N, b0, nloc, c->params[0], c->params[1] * c->params[1], terms + 2 * b0);
+        if (c->nccl_comm && (rc = nccl_allgather_inplace(c, terms, (size_t)(2 * nloc), st))) return rc;
+        irk::nbd_energy_sum_kernel<<<1, 1, 0, st>>>(terms, P, nloc, H);
         break;
     }
     case IRK_FPU_BETA: {
@@ -650,12 +770,32 @@ int irk_tableau(double *c, double *b, double *mu, double *nu) {
     return IRK_OK;
 }
 
+int irk_nccl_unique_id(void *out) {
+    if (!out) return IRK_E_ARG;
+    if (load_nccl()) return IRK_E_COMM;
+    ncclUniqueId id;
+    if (g_nccl.getUniqueId(&id) != ncclSuccess) return IRK_E_COMM;
+    memcpy(out, &id, sizeof id);
+    return IRK_OK;
+}
+
 int irk_set_comm(irk_ctx *c, const void *id, int rank, int nranks) {
     if (!c) return IRK_E_ARG;
-    (void)id;
-    (void)rank;
-    (void)nranks;
-    return fail(c, IRK_E_STATE, "irk_set_comm: body-sharded N-body not built yet");
+    if (c->problem != IRK_NBODY_DIRECT) return fail(c, IRK_E_ARG, "irk_set_comm: only IRK_NBODY_DIRECT shards");
+    if (!id || nranks < 1 || rank < 0 || rank >= nranks) return fail(c, IRK_E_ARG, "irk_set_comm: bad rank/nranks");
+    if ((c->dim / 6) % nranks) return fail(c, IRK_E_ARG, "irk_set_comm: N must be divisible by nranks");
+    if (c->nccl_comm) return fail(c, IRK_E_STATE, "irk_set_comm: communicator already set");
+    if (const char *e = load_nccl()) return fail(c, IRK_E_COMM, "irk_set_comm: %s", e);
+    ncclUniqueId uid;
+    memcpy(&uid, id, sizeof uid);
+    ncclComm_t comm = nullptr;
+    int rc = nccl_check(c, g_nccl.commInitRank(&comm, nranks, uid, rank), "ncclCommInitRank");
+    if (rc) return rc;
+    c->nccl_comm = comm;
+    c->nranks = nranks;
+    c->rank = rank;
+    c->vshards = 1;
+    return IRK_OK;
 }
 
 const char *irk_last_error(const irk_ctx *c) {
@@ -671,6 +811,7 @@ void irk_destroy(irk_ctx *c) {
     cudaFree(c->d_ws);
     cudaFree(c->d_mass);
     cudaFree(c->d_rows);
+    if (c->nccl_comm && g_nccl.commDestroy) g_nccl.commDestroy(reinterpret_cast<ncclComm_t>(c->nccl_comm));
     if (c->h_ctl) cudaFreeHost(c->h_ctl);
     delete c;
 }

@@ -1,23 +1,30 @@
-// Large-N single-system path (config 5, IRK_NBODY_DIRECT): one gravitational
-// system of N bodies (d = 3N position components), all 8 stages, split into
-// three kernels per fixed-point sweep plus a one-thread control kernel:
+// Large-N single-system path (config 5, IRK_NBODY_DIRECT), body-sharded.
 //
-//   nbd_pos    (a2 + a5)  component-parallel: Lq = hb o V, Q_i = q + D(mu_i, Lq),
-//                         Delta vs Q^[k-1], stop-test state (m, p) per component,
-//                         a global "not converged" flag.
-//   nbd_force  (a3)       (stage, body, j-block) parallel: the canonical blocked
-//                         direct sum (R-8): one thread = one partial sum
-//                         over a block of NBD_JBLOCK = 1024 bodies j, with the
-//                         block's positions and masses staged in shared memory
-//                         (every lane reads the same j: broadcast).
-//   nbd_vel    (a4 + a6)  component-parallel: acc = ((0 + P_0) + P_1) + ... (blocks
-//                         left to right), Lv = hb o acc, then either V = v + D(mu, Lv)
-//                         or, when the step converged, the update q += S(Lq),
-//                         v += S(Lv), history <- Lv and the next nu-init.
-//   nbd_ctl    (1 thread) advances the sweep / step counters.
+// One gravitational system of N bodies split into P shards of nloc = N/P
+// bodies (P = 1 on one GPU; P = nranks under NCCL; or P "virtual" shards driven
+// by one process on one GPU to exercise the sharded layout).  Per fixed-point
+// sweep, per shard:
 //
-// All arithmetic follows the oracle's canonical sequence (accel_direct_body and
-// step_partitioned), so the result is bitwise the oracle's for any N.
+//   nbd_pos    (a2 + a5)  component-parallel over the shard's 3*nloc components:
+//                         Lq = hb o V, Q_i = q + D(mu_i, Lq), Delta vs Q^[k-1],
+//                         stop-test state (m, p); the shard's Q^[k] is written
+//                         straight into its slot of the gathered buffer Qg, plus
+//                         a "not converged" flag at the end of the slot.
+//   (exchange)            ncclAllGather in place on Qg (NCCL mode) -- the one
+//                         data-path collective, once per iteration;
+//                         nothing to do for virtual shards (shared buffer).
+//   nbd_or                global stop = no flag set in any slot (same on every rank).
+//   nbd_force  (a3)       (local body, stage, j-block) parallel: the canonical blocked
+//                         direct sum (R-8) over ALL N bodies read from Qg,
+//                         one thread = one partial sum over NBD_JBLOCK = 1024 bodies j
+//                         staged in shared memory (broadcast reads).
+//   nbd_vel    (a4 + a6)  acc = ((0 + P_0) + P_1) + ... , Lv = hb o acc, then
+//                         V = v + D(mu, Lv) or (converged) update + history + nu-init.
+//   nbd_ctl    (1 thread) sweep / step counters (identical decisions on all ranks).
+//
+// The arithmetic is the oracle's canonical sequence (accel_direct_body,
+// step_partitioned); the j-order does not depend on P, so every P gives the same
+// bits as the oracle.
 #pragma once
 #include <cstdint>
 
@@ -29,60 +36,75 @@ namespace irk {
 constexpr int NBD_JBLOCK = 1024;  // canonical j-block (oracle NB_BLOCK)
 constexpr int NBD_FORCE_THREADS = 128;
 
-struct NbdCtl {           // device-side control block (in the workspace)
+struct NbdCtl {           // device-side control block (one per process)
     int64_t n;            // steps completed in this call
     int32_t k;            // sweeps completed in the current step
-    int32_t notok;        // any component failed the stop test in this sweep
-    int32_t fin;          // last sweep finished a step (for the host / energy)
-    int32_t nonfinite;    // a component became non-finite at the last update
-    int64_t sweeps, hits, bad;
+    int32_t notok;        // global: some component failed the stop test this sweep
+    int32_t fin;          // last sweep finished a step
+    int32_t nonfinite;    // global (after an exchange): some component became non-finite
+    int32_t halt;         // stop integrating (divergence)
+    int32_t pad;
+    int64_t sweeps, hits;
 };
 
+// Per-shard arguments.  Component index l in [0, 3*nloc) of shard s is global
+// position component 3*b0 + l.
 struct NbdArgs {
     double hb[8];
-    double *y;            // [6N] (batch = 1): q then v
-    double *hist;         // [8][6N]
-    double *Q;            // [8][3N]
-    double *V;            // [8][3N]
-    double *M, *Pst;      // [3N] stop-test state
-    double *sLq;          // [3N]
-    double *part;         // [nj][8][3N] block partial sums
+    double *yq, *yv;      // shard's q and v blocks (3*nloc each)
+    double *hist;         // history base; rows j*hdim + hq + l (q block), j*hdim + hv + l (v block)
+    int64_t hdim, hq, hv;
+    double *Qg;           // gathered stage positions [P][stride]; slot s = [8][3*nloc] + 2 flags
+    int64_t stride;       // doubles per slot (8*3*nloc + 2): flags {not converged, non-finite}
+    double *V;            // [8][3*nloc]
+    double *M, *Pst;      // [3*nloc] stop-test state
+    double *sLq;          // [3*nloc]
+    double *part;         // [nj][8][3*nloc] block partial sums
     const double *mass;   // [N]
     NbdCtl *ctl;
-    int64_t nbody, nsteps;
+    int64_t nbody, nloc, b0;
+    int shard, nshards;
     double G, eps2;
     int max_iters;
 };
 
+__device__ __forceinline__ double *nbd_slot(const NbdArgs &a, int s) { return a.Qg + (int64_t)s * a.stride; }
+__device__ __forceinline__ int64_t nbd_flag_index(const NbdArgs &a) { return 24 * a.nloc; }
+
 __global__ void nbd_init_kernel(const __grid_constant__ NbdArgs a) {
-    const int64_t d = 3 * a.nbody;
+    const int64_t dl = 3 * a.nloc;
     const int64_t l = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (l >= d) return;
+    if (l == 0) {
+        nbd_slot(a, a.shard)[nbd_flag_index(a)] = 0.0;
+        nbd_slot(a, a.shard)[nbd_flag_index(a) + 1] = 0.0;
+    }
+    if (l >= dl) return;
     const double kInf = __longlong_as_double(0x7ff0000000000000LL);
-    const double v = a.y[d + l];
+    const double v = a.yv[l];
     double H[8];
 #pragma unroll
-    for (int j = 0; j < 8; ++j) H[j] = a.hist[(int64_t)j * 2 * d + d + l];
+    for (int j = 0; j < 8; ++j) H[j] = a.hist[(int64_t)j * a.hdim + a.hv + l];
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
         double acc = dmul(c_nu[i][0], H[0]);
 #pragma unroll
         for (int j = 1; j < 8; ++j) acc = dfma(c_nu[i][j], H[j], acc);
-        a.V[(int64_t)i * d + l] = dadd(v, acc);
+        a.V[(int64_t)i * dl + l] = dadd(v, acc);
     }
     a.M[l] = kInf;
     a.Pst[l] = kInf;
 }
 
 __global__ void nbd_pos_kernel(const __grid_constant__ NbdArgs a) {
-    const int64_t d = 3 * a.nbody;
+    const int64_t dl = 3 * a.nloc;
     const int64_t l = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (l >= d) return;
+    if (l >= dl) return;
     const int k = a.ctl->k + 1;
-    const double q = a.y[l];
+    double *Q = nbd_slot(a, a.shard);
+    const double q = a.yq[l];
     double Lq[8];
 #pragma unroll
-    for (int j = 0; j < 8; ++j) Lq[j] = dmul(a.hb[j], a.V[(int64_t)j * d + l]);
+    for (int j = 0; j < 8; ++j) Lq[j] = dmul(a.hb[j], a.V[(int64_t)j * dl + l]);
     double s = Lq[0];
 #pragma unroll
     for (int j = 1; j < 8; ++j) s = dadd(s, Lq[j]);
@@ -94,9 +116,9 @@ __global__ void nbd_pos_kernel(const __grid_constant__ NbdArgs a) {
 #pragma unroll
         for (int j = 1; j < 8; ++j) acc = dfma(c_mu[i][j], Lq[j], acc);
         const double qn = dadd(q, acc);
-        const double e = dabs(dsub(qn, a.Q[(int64_t)i * d + l]));
+        const double e = dabs(dsub(qn, Q[(int64_t)i * dl + l]));
         delta = (e > delta) ? e : delta;
-        a.Q[(int64_t)i * d + l] = qn;
+        Q[(int64_t)i * dl + l] = qn;
     }
     if (k >= 2) {
         const double pl = a.Pst[l], ml = a.M[l];
@@ -104,26 +126,38 @@ __global__ void nbd_pos_kernel(const __grid_constant__ NbdArgs a) {
         const bool ok = (delta == 0.0) || (ml <= mn);
         a.M[l] = (pl < ml) ? pl : ml;
         a.Pst[l] = delta;
-        if (!ok) a.ctl->notok = 1;  // benign race: every writer stores 1
+        if (!ok) Q[nbd_flag_index(a)] = 1.0;  // benign race: every writer stores 1
     }
 }
 
-// grid: x = body tile (NBD_FORCE_THREADS bodies), y = stage i, z = j-block
+// global flags from every slot (after the exchange)
+__global__ void nbd_or_kernel(const __grid_constant__ NbdArgs a) {
+    int any = 0, bad = 0;
+    for (int s = 0; s < a.nshards; ++s) {
+        any |= (nbd_slot(a, s)[nbd_flag_index(a)] != 0.0);
+        bad |= (nbd_slot(a, s)[nbd_flag_index(a) + 1] != 0.0);
+    }
+    a.ctl->notok = any;
+    a.ctl->nonfinite = bad;
+}
+
+// grid: x = local body tile (NBD_FORCE_THREADS bodies), y = stage i, z = j-block
 __global__ void __launch_bounds__(NBD_FORCE_THREADS) nbd_force_kernel(const __grid_constant__ NbdArgs a) {
     __shared__ double4 sj[NBD_JBLOCK];
-    const int64_t N = a.nbody, d = 3 * N;
+    const int64_t N = a.nbody, nloc = a.nloc, dl = 3 * nloc;
     const int i = blockIdx.y, J = blockIdx.z;
     const int64_t j0 = (int64_t)J * NBD_JBLOCK;
     const int nj = (int)((N - j0) < NBD_JBLOCK ? (N - j0) : NBD_JBLOCK);
-    const double *Qi = a.Q + (int64_t)i * d;
     for (int t = threadIdx.x; t < nj; t += blockDim.x) {
         const int64_t j = j0 + t;
-        sj[t] = make_double4(Qi[3 * j], Qi[3 * j + 1], Qi[3 * j + 2], a.mass[j]);
+        const double *Qj = nbd_slot(a, (int)(j / nloc)) + (int64_t)i * dl + 3 * (j % nloc);
+        sj[t] = make_double4(Qj[0], Qj[1], Qj[2], a.mass[j]);
     }
     __syncthreads();
-    const int64_t body = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (body >= N) return;
-    const double qx = Qi[3 * body], qy = Qi[3 * body + 1], qz = Qi[3 * body + 2];
+    const int64_t body = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;  // local index
+    if (body >= nloc) return;
+    const double *Qa = nbd_slot(a, a.shard) + (int64_t)i * dl + 3 * body;
+    const double qx = Qa[0], qy = Qa[1], qz = Qa[2];
     double px = 0.0, py = 0.0, pz = 0.0;
     bool ok = true;
 #pragma unroll 4
@@ -137,7 +171,7 @@ __global__ void __launch_bounds__(NBD_FORCE_THREADS) nbd_force_kernel(const __gr
         py = dfma(s, dy, py);
         pz = dfma(s, dz, pz);
     }
-    if (!ok) {  // some operand outside the fast-path range: exact intrinsics, same bits
+    if (!ok) {  // an operand outside the fast-path range: exact intrinsics, same bits
         px = py = pz = 0.0;
         for (int t = 0; t < nj; ++t) {
             const double4 pj = sj[t];
@@ -150,16 +184,17 @@ __global__ void __launch_bounds__(NBD_FORCE_THREADS) nbd_force_kernel(const __gr
             pz = dfma(s, dz, pz);
         }
     }
-    double *P = a.part + ((int64_t)J * 8 + i) * d;
+    double *P = a.part + ((int64_t)J * 8 + i) * dl;
     P[3 * body] = px;
     P[3 * body + 1] = py;
     P[3 * body + 2] = pz;
 }
 
 __global__ void nbd_vel_kernel(const __grid_constant__ NbdArgs a) {
-    const int64_t d = 3 * a.nbody;
+    const int64_t dl = 3 * a.nloc;
     const int64_t l = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (l >= d) return;
+    if (l >= dl) return;
+    if (a.ctl->nonfinite) return;  // diverged at the previous step: frozen (R-10)
     const int nj = (int)((a.nbody + NBD_JBLOCK - 1) / NBD_JBLOCK);
     const int k = a.ctl->k + 1;
     const bool stop = (k >= 2) && (a.ctl->notok == 0);
@@ -168,23 +203,23 @@ __global__ void nbd_vel_kernel(const __grid_constant__ NbdArgs a) {
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
         double acc = 0.0;
-        for (int J = 0; J < nj; ++J) acc = dadd(acc, a.part[((int64_t)J * 8 + i) * d + l]);
+        for (int J = 0; J < nj; ++J) acc = dadd(acc, a.part[((int64_t)J * 8 + i) * dl + l]);
         Lv[i] = dmul(a.hb[i], acc);
     }
-    double v = a.y[d + l];
+    double v = a.yv[l];
     if (fin) {
         double sv = Lv[0];
 #pragma unroll
         for (int j = 1; j < 8; ++j) sv = dadd(sv, Lv[j]);
-        const double q = dadd(a.y[l], a.sLq[l]);
+        const double q = dadd(a.yq[l], a.sLq[l]);
         v = dadd(v, sv);
-        a.y[l] = q;
-        a.y[d + l] = v;
-        if (!isfinite(q) || !isfinite(v)) a.ctl->nonfinite = 1;
+        a.yq[l] = q;
+        a.yv[l] = v;
+        if (!isfinite(q) || !isfinite(v)) nbd_slot(a, a.shard)[nbd_flag_index(a) + 1] = 1.0;
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
-            a.hist[(int64_t)j * 2 * d + l] = 0.0;
-            a.hist[(int64_t)j * 2 * d + d + l] = Lv[j];
+            a.hist[(int64_t)j * a.hdim + a.hq + l] = 0.0;
+            a.hist[(int64_t)j * a.hdim + a.hv + l] = Lv[j];
         }
         const double kInf = __longlong_as_double(0x7ff0000000000000LL);
         a.M[l] = kInf;
@@ -195,12 +230,21 @@ __global__ void nbd_vel_kernel(const __grid_constant__ NbdArgs a) {
         double acc = dmul(fin ? c_nu[i][0] : c_mu[i][0], Lv[0]);
 #pragma unroll
         for (int j = 1; j < 8; ++j) acc = dfma(fin ? c_nu[i][j] : c_mu[i][j], Lv[j], acc);
-        a.V[(int64_t)i * d + l] = dadd(v, acc);
+        a.V[(int64_t)i * dl + l] = dadd(v, acc);
     }
 }
 
-__global__ void nbd_ctl_kernel(const __grid_constant__ NbdArgs a, int64_t *n_done, int64_t *stats) {
+// after the last shard's nbd_vel of the sweep: counters, stats, reset local flags
+__global__ void nbd_ctl_kernel(const __grid_constant__ NbdArgs a, int first_local, int nlocal, int64_t *n_done,
+                               int64_t *stats) {
     NbdCtl *c = a.ctl;
+    for (int s = first_local; s < first_local + nlocal; ++s) nbd_slot(a, s)[nbd_flag_index(a)] = 0.0;
+    if (c->nonfinite) {  // some shard diverged at the last completed step
+        if (stats[1] == 0) stats[1] = *n_done;
+        c->halt = 1;
+        c->fin = 0;
+        return;
+    }
     const int k = c->k + 1;
     const bool stop = (k >= 2) && (c->notok == 0);
     const bool fin = stop || (k >= a.max_iters);
@@ -214,20 +258,30 @@ __global__ void nbd_ctl_kernel(const __grid_constant__ NbdArgs a, int64_t *n_don
         *n_done += 1;
         stats[0] += stop ? 0 : 1;
         stats[2] += k;
-        if (c->nonfinite && stats[1] == 0) stats[1] = *n_done;
     } else {
         c->k = k;
     }
 }
 
-// H of the system (canonical: kinetic terms, then row sums over j > i, Neumaier).
-// Pass 1: one thread per row i writes its Neumaier row sum; pass 2 (one thread)
-// adds the kinetic terms and the rows in order.
-__global__ void nbd_energy_rows_kernel(const double *y, const double *mass, int64_t N, double G, double eps2,
-                                       double *rows) {
-    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (i >= N) return;
-    const double *q = y;
+// after the final exchange of a call: record a divergence at the last step
+__global__ void nbd_final_kernel(const __grid_constant__ NbdArgs a, int64_t *n_done, int64_t *stats) {
+    int bad = 0;
+    for (int s = 0; s < a.nshards; ++s) bad |= (nbd_slot(a, s)[nbd_flag_index(a) + 1] != 0.0);
+    if (bad && stats[1] == 0) stats[1] = *n_done;
+}
+
+// ---- energy (canonical: kinetic terms, then row sums over j > i, Neumaier) ----
+// Qall: all N positions (3N, gathered); each shard writes its kinetic terms and
+// row sums into its slot [kin(nloc) | row(nloc)] of `terms` ([P][2*nloc]); the
+// total is added by one thread over all kinetic terms, then all rows, in order.
+__global__ void nbd_energy_terms_kernel(const double *Qall, const double *vloc, const double *mass, int64_t N,
+                                        int64_t b0, int64_t nloc, double G, double eps2, double *slot) {
+    const int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (r >= nloc) return;
+    const int64_t i = b0 + r;
+    const double *q = Qall, *v = vloc + 3 * r;
+    const double k = dfma(v[2], v[2], dfma(v[1], v[1], dmul(v[0], v[0])));
+    slot[r] = dmul(dmul(0.5, mass[i]), k);
     Neumaier row;
     for (int64_t j = i + 1; j < N; ++j) {
         const double dx = dsub(q[3 * j], q[3 * i]);
@@ -236,18 +290,15 @@ __global__ void nbd_energy_rows_kernel(const double *y, const double *mass, int6
         const double r2 = dfma(dz, dz, dfma(dy, dy, dfma(dx, dx, eps2)));
         row.add(-ddiv(dmul(G, dmul(mass[i], mass[j])), dsqrt(r2)));
     }
-    rows[i] = row.result();
+    slot[nloc + r] = row.result();
 }
 
-__global__ void nbd_energy_sum_kernel(const double *y, const double *mass, int64_t N, const double *rows,
-                                      double *out) {
-    const double *v = y + 3 * N;
+__global__ void nbd_energy_sum_kernel(const double *terms, int P, int64_t nloc, double *out) {
     Neumaier tot;
-    for (int64_t i = 0; i < N; ++i) {
-        const double k = dfma(v[3 * i + 2], v[3 * i + 2], dfma(v[3 * i + 1], v[3 * i + 1], dmul(v[3 * i], v[3 * i])));
-        tot.add(dmul(dmul(0.5, mass[i]), k));
-    }
-    for (int64_t i = 0; i < N; ++i) tot.add(rows[i]);
+    for (int s = 0; s < P; ++s)
+        for (int64_t r = 0; r < nloc; ++r) tot.add(terms[(int64_t)s * 2 * nloc + r]);
+    for (int s = 0; s < P; ++s)
+        for (int64_t r = 0; r < nloc; ++r) tot.add(terms[(int64_t)s * 2 * nloc + nloc + r]);
     *out = tot.result();
 }
 

@@ -14,7 +14,7 @@ import numpy as np
 
 KEPLER, NBODY, FPU_BETA, HENON_HEILES, NBODY_DIRECT = 1, 2, 3, 4, 5
 OK, W_MAXITER, E_ARG, E_CUDA, E_DIVERGED, E_COMM, E_STATE = 0, 1, -1, -2, -3, -4, -5
-OPT_MODE, OPT_MAX_ITERS, OPT_ENERGY_EVERY, OPT_MAPPING, OPT_BALANCE = 1, 2, 3, 4, 5
+OPT_MODE, OPT_MAX_ITERS, OPT_ENERGY_EVERY, OPT_MAPPING, OPT_BALANCE, OPT_VSHARDS = 1, 2, 3, 4, 5, 6
 PARTITIONED, FIRST_ORDER = 0, 1
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
@@ -22,7 +22,7 @@ LIB_PATH = os.environ.get("IRK_LIB_OVERRIDE") or os.path.join(_HERE, "lib", "lib
 
 SYMBOLS = ["irk_create", "irk_set_params", "irk_set_option", "irk_workspace_bytes",
            "irk_integrate", "irk_integrate_host", "irk_energy", "irk_stats", "irk_tableau",
-           "irk_set_comm", "irk_last_error", "irk_destroy", "irk_probe_dfma",
+           "irk_set_comm", "irk_nccl_unique_id", "irk_last_error", "irk_destroy", "irk_probe_dfma",
            "irk_probe_divsqrt"]
 
 _lib = None
@@ -57,6 +57,7 @@ def lib():
             l.irk_stats.argtypes = [vp, vp, vp, i64p]
             l.irk_tableau.argtypes = [dp, dp, dp, dp]
             l.irk_set_comm.argtypes = [vp, vp, ctypes.c_int, ctypes.c_int]
+            l.irk_nccl_unique_id.argtypes = [vp]
             l.irk_last_error.argtypes = [vp]
             l.irk_last_error.restype = ctypes.c_char_p
             l.irk_destroy.argtypes = [vp]
@@ -89,7 +90,7 @@ class Integrator:
 
     def __init__(self, problem: int, dim: int, h: float, nsteps: int, batch: int, params,
                  *, mode: int = PARTITIONED, max_iters: int = 100, energy_every: int = 0,
-                 mapping: int = 0, balance: int = -1):
+                 mapping: int = 0, balance: int = -1, vshards: int = 1):
         L = lib()
         self._ctx = L.irk_create(problem, dim, h, nsteps, batch)
         if not self._ctx:
@@ -102,6 +103,19 @@ class Integrator:
                          (OPT_ENERGY_EVERY, energy_every), (OPT_MAPPING, mapping),
                          (OPT_BALANCE, balance)):
             self._check(L.irk_set_option(self._ctx, key, val))
+        if vshards != 1:
+            self._check(L.irk_set_option(self._ctx, OPT_VSHARDS, vshards))
+        self.rank, self.nranks = 0, 1
+
+    def set_comm(self, unique_id: bytes, rank: int, nranks: int):
+        """Body-shard an IRK_NBODY_DIRECT system over NCCL (include/irk.h irk_set_comm)."""
+        buf = ctypes.create_string_buffer(bytes(unique_id), 128)
+        self._check(lib().irk_set_comm(self._ctx, ctypes.cast(buf, ctypes.c_void_p), rank, nranks))
+        self.rank, self.nranks = rank, nranks
+
+    @property
+    def local_dim(self) -> int:
+        return self.dim // self.nranks
 
     def _check(self, rc):
         if rc < 0:
@@ -136,7 +150,7 @@ class Integrator:
         """Advance y in place on the device (irk_integrate); asynchronous on `stream`."""
         import torch
         assert y.dtype == torch.float64 and y.is_cuda and y.is_contiguous()
-        assert tuple(y.shape) == (self.dim, self.batch)
+        assert tuple(y.shape) == (self.local_dim, self.batch)
         assert workspace.numel() >= self.workspace_bytes
         s = torch.cuda.current_stream(y.device) if stream is None else stream
         self._check(lib().irk_integrate(self._ctx, _ptr(y), t0, _ptr(workspace), _ptr(energy),
@@ -147,7 +161,7 @@ class Integrator:
         """End-to-end call from host memory (irk_integrate_host); returns (energy, iters)."""
         import torch
         assert y_host.dtype == np.float64 and y_host.flags.c_contiguous
-        assert y_host.shape == (self.dim, self.batch)
+        assert y_host.shape == (self.local_dim, self.batch)
         E = np.zeros((self.n_energy(), self.batch)) if (want_energy and self.energy_every > 0) else None
         it = np.zeros(self.batch, dtype=np.int64) if want_iters else None
         s = torch.cuda.current_stream() if stream is None else stream
@@ -179,8 +193,8 @@ class Integrator:
     def hist_view(self, workspace):
         """The history block of a workspace as a float64 (8, dim, batch) tensor view."""
         import torch
-        nb = 8 * self.dim * self.batch * 8
-        return workspace[64:64 + nb].view(torch.float64).view(8, self.dim, self.batch)
+        nb = 8 * self.local_dim * self.batch * 8
+        return workspace[64:64 + nb].view(torch.float64).view(8, self.local_dim, self.batch)
 
 
 def probe_dfma(out, blocks: int, iters: int, stream) -> int:
@@ -200,3 +214,12 @@ def probe_divsqrt(a, b, stream=None):
     if lib().irk_probe_divsqrt(_ptr(a), _ptr(b), _ptr(out), n, ctypes.c_void_p(s.cuda_stream)):
         raise IrkError(E_CUDA, "irk_probe_divsqrt failed")
     return out
+
+
+def nccl_unique_id() -> bytes:
+    """128-byte ncclUniqueId for Integrator.set_comm (call on rank 0, broadcast)."""
+    buf = ctypes.create_string_buffer(128)
+    rc = lib().irk_nccl_unique_id(ctypes.cast(buf, ctypes.c_void_p))
+    if rc:
+        raise IrkError(rc, "irk_nccl_unique_id failed (NCCL not loadable?)")
+    return buf.raw

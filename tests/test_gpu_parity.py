@@ -373,3 +373,43 @@ def test_first_order_mode_parity(irk, orc):
         o = orc.integrate(w.problem, w.y, w.params, w.h, 600, mode=orc.FIRST_ORDER)
         assert np.array_equal(y, o["y"]) and np.array_equal(tot, o["iters"])
         assert np.array_equal(hist, o["hist"].transpose(1, 2, 0))
+
+
+def test_config5_virtual_shards_bitwise(irk, orc):
+    """The body-sharded code path (slot-major gathered stage positions, global
+    stop flag, per-shard force/vel) driven as P = 2, 4, 8 virtual shards on one
+    GPU equals the oracle bit for bit (the j-order does not depend on P)."""
+    w = wl.plummer(N=1024, nsteps=12)
+    o = orc.integrate(w.problem, w.y, w.params, w.h, w.nsteps, energy_every=4)
+    for P in (2, 4, 8):
+        with irk.Integrator(w.problem, w.dim, w.h, w.nsteps, 1, w.params, energy_every=4, vshards=P) as ig:
+            Y = torch.tensor(w.y, dtype=torch.float64, device="cuda")
+            ws = ig.new_workspace()
+            E = torch.zeros((ig.n_energy(), 1), dtype=torch.float64, device="cuda")
+            it = torch.zeros(1, dtype=torch.int64, device="cuda")
+            ig.integrate(Y, ws, energy=E, iters=it)
+            assert np.array_equal(Y.cpu().numpy(), o["y"]), P
+            assert np.array_equal(E.cpu().numpy(), o["energy"]), P
+            assert int(it.item()) == int(o["iters"][0])
+
+
+def test_config5_nccl_single_rank_path(irk, orc):
+    """irk_set_comm with one rank: the NCCL exchange (in-place ncclAllGather per
+    iteration, energy gathers) runs and the result is bitwise the oracle's."""
+    import torch.distributed as dist
+    w = wl.plummer(N=512, nsteps=6)
+    o = orc.integrate(w.problem, w.y, w.params, w.h, w.nsteps, energy_every=3)
+    try:
+        uid = irk.nccl_unique_id()
+    except irk.IrkError:
+        pytest.skip("NCCL not loadable")
+    with irk.Integrator(w.problem, w.dim, w.h, w.nsteps, 1, w.params, energy_every=3) as ig:
+        ig.set_comm(uid, 0, 1)
+        Y = torch.tensor(w.y, dtype=torch.float64, device="cuda")
+        ws = ig.new_workspace()
+        E = torch.zeros((ig.n_energy(), 1), dtype=torch.float64, device="cuda")
+        ig.integrate(Y, ws, energy=E)
+        H = ig.energy(Y).cpu().numpy()
+        assert np.array_equal(Y.cpu().numpy(), o["y"])
+        assert np.array_equal(E.cpu().numpy(), o["energy"])
+        assert H[0] == orc.energy(w.problem, w.dim, w.params, o["y"][:, 0])

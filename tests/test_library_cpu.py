@@ -97,3 +97,12 @@ def test_build_is_sm100a_only(irk):
     out = subprocess.run([exe, "--list-elf", irk.LIB_PATH], capture_output=True, text=True).stdout
     archs = set(re.findall(r"sm_(\d+a?)", out))
     assert archs == {"100a"}, archs
+
+
+def test_nccl_unique_id_loads_nccl_at_run_time(irk):
+    """irk_nccl_unique_id dlopens NCCL (no link-time dependency) and returns 128 bytes."""
+    try:
+        u = irk.nccl_unique_id()
+    except irk.IrkError:
+        pytest.skip("NCCL not loadable here")
+    assert len(u) == 128 and u != bytes(128)
