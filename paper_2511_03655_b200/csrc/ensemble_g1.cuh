@@ -29,6 +29,9 @@ constexpr int G1_THREADS = 64;
 #ifndef G1_MAXREG
 #define G1_MAXREG 168    // measured best on config 2 (tools/variants.py): 128: 116 ms, 144: 136, 168: 107, 190+: 109-111
 #endif
+#ifndef G1_V_SMEM
+#define G1_V_SMEM 0      // keep V^[k] in shared memory instead of registers
+#endif
 #ifndef G1_RHS_ILP
 #define G1_RHS_ILP 8     // stages per trip of the RHS loop (8: 107 ms, 4: 145 ms at 168 regs)
 #endif
@@ -54,7 +57,14 @@ __global__ void __maxnreg__(G1_MAXREG) ens_g1_kernel(const __grid_constant__ Ens
     // and the RHS temporaries (ILP across the eight stages).
     __shared__ double sQ[8 * d][G1_THREADS], sL[8 * d][G1_THREADS], sM[d][G1_THREADS], sP[d][G1_THREADS];
     const int tx = threadIdx.x;
-    double q[d], v[d], V[8][d];
+#if G1_V_SMEM
+    __shared__ double sV[8 * d][G1_THREADS];  // V^[k] between a4 and the next a2
+#define G1_V(i, l) sV[(i) * d + (l)][tx]
+#else
+    double V[8][d];
+#define G1_V(i, l) V[i][l]
+#endif
+    double q[d], v[d];
 #pragma unroll
     for (int l = 0; l < d; ++l) {
         q[l] = a.y[l * B + b];
@@ -81,7 +91,7 @@ __global__ void __maxnreg__(G1_MAXREG) ens_g1_kernel(const __grid_constant__ Ens
                 double acc = dmul(c_nu[i][0], H[0][l]);
 #pragma unroll
                 for (int j = 1; j < 8; ++j) acc = dfma(c_nu[i][j], H[j][l], acc);
-                V[i][l] = dadd(v[l], acc);
+                G1_V(i, l) = dadd(v[l], acc);
             }
     }
     const double kInf = __longlong_as_double(0x7ff0000000000000LL);
@@ -99,7 +109,7 @@ __global__ void __maxnreg__(G1_MAXREG) ens_g1_kernel(const __grid_constant__ Ens
 #pragma unroll
         for (int j = 0; j < 8; ++j)
 #pragma unroll
-            for (int l = 0; l < d; ++l) Lq[j][l] = dmul(a.hb[j], V[j][l]);
+            for (int l = 0; l < d; ++l) Lq[j][l] = dmul(a.hb[j], G1_V(j, l));
 #pragma unroll
         for (int l = 0; l < d; ++l) {
             sLq[l] = Lq[0][l];
@@ -108,9 +118,8 @@ __global__ void __maxnreg__(G1_MAXREG) ens_g1_kernel(const __grid_constant__ Ens
         }
         bool stop = (k >= 2);
         double delta[d];
-#pragma unroll
-        for (int l = 0; l < d; ++l) delta[l] = 0.0;
         {
+            double ev[d][8];
             const double2 *M = reinterpret_cast<const double2 *>(&c_mu[0][0]);
 #pragma unroll
             for (int i = 0; i < 8; ++i) {
@@ -127,11 +136,12 @@ __global__ void __maxnreg__(G1_MAXREG) ens_g1_kernel(const __grid_constant__ Ens
                         acc = dfma(w[jj].y, Lq[2 * jj + 1][l], acc);
                     }
                     const double qn = dadd(q[l], acc);
-                    const double e = dabs(dsub(qn, sQ[i * d + l][tx]));  // garbage at k = 1, unused
-                    delta[l] = (e > delta[l]) ? e : delta[l];
+                    ev[l][i] = dabs(dsub(qn, sQ[i * d + l][tx]));  // garbage at k = 1, unused
                     sQ[i * d + l][tx] = qn;
                 }
             }
+#pragma unroll
+            for (int l = 0; l < d; ++l) delta[l] = delta_max8(ev[l]);
         }
         if (k >= 2) {  // a5, reading R2: Delta^[k] exists from k = 2
 #pragma unroll
@@ -147,6 +157,38 @@ __global__ void __maxnreg__(G1_MAXREG) ens_g1_kernel(const __grid_constant__ Ens
         // a3 + a4 (first half): F_i = g(Q_i, t_i) ; Lv_i = hb_i F_i, G1_RHS_ILP stages per
         // trip (ILP for the ~20-deep dependent div/sqrt chains, bounded register use).
         const double tn1 = dadd(a.t0, dmul((double)(n0 + n), a.h));
+        double Lv[8][d];
+#if G1_RHS_ILP == 8
+        {   // all eight stages in flight, results straight into registers
+            bool ok = true;
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                double Qi[d];
+#pragma unroll
+                for (int l = 0; l < d; ++l) Qi[l] = sQ[i * d + l][tx];
+                prob.template accel<false>(Qi, Lv[i], dadd(tn1, dmul(c_c[i], a.h)), ok);
+            }
+            if (!ok) {  // some stage needs the exact slow path of div/sqrt: redo all, same bits
+#pragma unroll 1
+                for (int i = 0; i < 8; ++i) {
+                    double Qi[d], Fi[d];
+#pragma unroll
+                    for (int l = 0; l < d; ++l) Qi[l] = sQ[i * d + l][tx];
+                    prob.template accel<true>(Qi, Fi, dadd(tn1, dmul(c_c[i], a.h)), ok);
+#pragma unroll
+                    for (int l = 0; l < d; ++l) sL[i * d + l][tx] = Fi[l];
+                }
+#pragma unroll
+                for (int i = 0; i < 8; ++i)
+#pragma unroll
+                    for (int l = 0; l < d; ++l) Lv[i][l] = sL[i * d + l][tx];
+            }
+#pragma unroll
+            for (int i = 0; i < 8; ++i)
+#pragma unroll
+                for (int l = 0; l < d; ++l) Lv[i][l] = dmul(a.hb[i], Lv[i][l]);
+        }
+#else
         {
             bool ok = true;
 #pragma unroll 1
@@ -173,11 +215,11 @@ __global__ void __maxnreg__(G1_MAXREG) ens_g1_kernel(const __grid_constant__ Ens
                 }
             }
         }
-        double Lv[8][d];
 #pragma unroll
         for (int i = 0; i < 8; ++i)
 #pragma unroll
             for (int l = 0; l < d; ++l) Lv[i][l] = sL[i * d + l][tx];
+#endif
         const bool fin = stop || (k >= a.max_iters);
         if (fin) {  // a6: update with the last iteration's L, history <- Lv
             bool finite = true;
@@ -231,11 +273,12 @@ __global__ void __maxnreg__(G1_MAXREG) ens_g1_kernel(const __grid_constant__ Ens
                         acc = dfma(w[jj].x, Lv[2 * jj][l], acc);
                         acc = dfma(w[jj].y, Lv[2 * jj + 1][l], acc);
                     }
-                    V[i][l] = dadd(v[l], acc);
+                    G1_V(i, l) = dadd(v[l], acc);
                 }
             }
         }
     }
+#undef G1_V
 #pragma unroll
     for (int l = 0; l < d; ++l) {
         a.y[l * B + b] = q[l];

@@ -7,7 +7,8 @@ import sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
-VARIANTS = json.loads(os.environ.get("IRK_VARIANTS", "{}"))
+_VF = os.path.join(os.path.dirname(os.path.abspath(__file__)), "variants_current.json")
+VARIANTS = json.loads(os.environ.get("IRK_VARIANTS") or (open(_VF).read() if os.path.exists(_VF) else "{}"))
 
 
 def build_all():
@@ -45,6 +46,8 @@ print({name!r}, 'ms', min(ts[1:]), ts)
 
 if __name__ == "__main__":
     if sys.argv[1] == "build":
+        if os.environ.get("IRK_VARIANTS"):
+            open(_VF, "w").write(os.environ["IRK_VARIANTS"])
         build_all()
     else:
         for n in VARIANTS:
