@@ -62,8 +62,16 @@ __device__ double nbody_energy(const double *qv, const NBodyParams &P) {
     return tot.result();
 }
 
+#ifndef NB_MAXREG
+#define NB_MAXREG 168  // config 3, 5,000 steps: 168 -> 306 ms, 255 -> 309, 128 -> 342 (tools/variants.py)
+#endif
+#ifndef NB_RHS_UNROLL
+#define NB_RHS_UNROLL 2  // stages of the RHS loop in flight
+#endif
+constexpr int kNbRhsUnroll = NB_RHS_UNROLL;
+
 template <int NB>
-__global__ void __launch_bounds__(NB_THREADS) ens_nbody_kernel(const __grid_constant__ EnsArgs a,
+__global__ void __maxnreg__(NB_MAXREG) ens_nbody_kernel(const __grid_constant__ EnsArgs a,
                                                                const __grid_constant__ NBodyParams P) {
     constexpr int GPW = 32 / NB;                 // groups (trajectories) per warp
     constexpr int GPB = GPW * (NB_THREADS / 32);  // groups per block
@@ -208,7 +216,7 @@ __global__ void __launch_bounds__(NB_THREADS) ens_nbody_kernel(const __grid_cons
         const double tn1 = dadd(a.t0, dmul((double)(n0 + n), a.h));
         (void)tn1;  // the N-body RHS is autonomous
         bool okdiv = true;
-#pragma unroll 2
+#pragma unroll kNbRhsUnroll
         for (int i = 0; i < 8; ++i) {
             const double *Qi = sQ[gib][i];
             const double qx = Qi[3 * body], qy = Qi[3 * body + 1], qz = Qi[3 * body + 2];

@@ -18,8 +18,14 @@ def build_all():
         build.build(force=True, out=out, defines=tuple(defs))
         log = open(out + ".ptxas.log").read()
         import re
-        m = re.findall(r"ens_g1_kernelINS_6Kepler.*?\n(.*?)\n(.*?)\n", log, re.S)
-        print(name, m[0] if m else "")
+        for kern in ("ens_g1_kernelINS_6Kepler", "ens_nbody_kernelILi6", "ens_chain_kernelILi2"):
+            m = re.search(r"Compiling entry function '_ZN3irk\d+" + kern + r".*?\n.*?\n(.*?)\n(.*?)\n", log, re.S)
+            if m:
+                print(name, kern, m.group(1).strip(), "|", m.group(2).strip()[:60])
+
+
+CFG = int(os.environ.get("IRK_VARIANT_CONFIG", "2"))
+NSTEPS = int(os.environ.get("IRK_VARIANT_NSTEPS", "0"))
 
 
 def time_one(name):
@@ -29,7 +35,7 @@ import os, sys, torch
 os.environ['IRK_LIB_OVERRIDE'] = {lib!r}
 sys.path.insert(0, {ROOT!r})
 from paper_2511_03655_b200 import irk, workloads as wl
-w = wl.kepler_ensemble()
+w = wl.config({CFG}, **({{'nsteps': {NSTEPS}}} if {NSTEPS} else {{}}))
 ig = irk.Integrator(w.problem, w.dim, w.h, w.nsteps, w.batch, w.params)
 y0 = torch.tensor(w.y, device='cuda'); Y = torch.empty_like(y0); ws = ig.new_workspace()
 ts = []
