@@ -109,7 +109,7 @@ struct Sched {
     int32_t *perm, *csweeps, *sorted, *bins;
 };
 // thread-slot capacity of the scheduler's permutation (>= slots of any ensemble kernel)
-int64_t perm_slots(int64_t B) { return (B + 63) / 64 * 64; }
+int64_t perm_slots(int64_t B) { return (B + 255) / 256 * 256; }  // >= slots of every mapping
 size_t sched_bytes(const irk_ctx *c) {
     return sizeof(int32_t) * ((size_t)perm_slots(c->batch) + 2 * (size_t)c->batch + irk::kCostBins);
 }
@@ -566,7 +566,7 @@ int irk_set_option(irk_ctx *c, int key, int64_t val) {
         c->vshards = (int)val;
         return IRK_OK;
     case IRK_OPT_MAPPING:
-        if (val < 0) return fail(c, IRK_E_ARG, "irk_set_option: bad MAPPING");
+        if (val < 0 || val > 1) return fail(c, IRK_E_ARG, "irk_set_option: MAPPING must be 0 (auto) or 1");
         c->mapping = (int)val;
         return IRK_OK;
     }
