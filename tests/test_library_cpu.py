@@ -83,7 +83,7 @@ def test_params_and_options_errors(irk):
         irk.Integrator(irk.FPU_BETA, 128, 0.1, 10, 4, params=[1.0], mode=irk.FIRST_ORDER)
     irk.Integrator(irk.HENON_HEILES, 4, 0.1, 10, 4, params=[1.0, 0.0], mode=irk.FIRST_ORDER).close()
     w = irk.Integrator(irk.KEPLER, 4, -0.1, 10, 4, params=[1.0])  # negative h is allowed
-    assert w.workspace_bytes == 64 + 8 * 8 * 4 * 4 + 8 * 4 * 4 + 4 * (64 + 2 * 4 + 1024)
+    assert w.workspace_bytes == 64 + 8 * 8 * 4 * 4 + 8 * 4 * 4 + 4 * (256 + 2 * 4 + 1024)
     w.close()
 
 
