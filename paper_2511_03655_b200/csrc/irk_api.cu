@@ -152,25 +152,32 @@ int run_chunks(irk_ctx *c, EnsArgs &a, char *ws, int64_t nblocks, int wpb, int s
         return cuda_check(c, cudaGetLastError(), "advance_n launch");
     }
     Sched sc = sched_of(c, ws);
-    for (int64_t c0 = 0; c0 < c->nsteps; c0 += chunk) {
-        const int64_t steps = (c->nsteps - c0 < chunk) ? c->nsteps - c0 : chunk;
+    // auto schedule: a short unsorted pilot chunk (1/4 of a chunk) measures the
+    // costs, then full chunks run cost-sorted; an explicit BALANCE = C uses C throughout
+    const int64_t pilot = (c->balance < 0) ? (chunk + 3) / 4 : chunk;
+    int64_t prev_steps = 0;
+    for (int64_t c0 = 0; c0 < c->nsteps;) {
+        const int64_t want = (c0 == 0) ? pilot : chunk;
+        const int64_t steps = (c->nsteps - c0 < want) ? c->nsteps - c0 : want;
         a.nsteps = steps;
         a.c0 = c0;
         a.csweeps = sc.csweeps;
         if (c0 == 0) {
             a.perm = nullptr;
             a.nslots = c->batch;
-        } else {  // sort by the previous chunk's sweeps, deal warps to blocks
+        } else {  // sort by the previous chunk's sweeps per step, deal warps to blocks
             const unsigned sb = (unsigned)((c->batch + 255) / 256 < 1184 ? (c->batch + 255) / 256 : 1184);
             cudaMemsetAsync(sc.bins, 0, sizeof(int32_t) * irk::kCostBins, st);
-            irk::cost_hist_kernel<<<sb, 256, 0, st>>>(sc.csweeps, c->batch, chunk, sc.bins);
+            irk::cost_hist_kernel<<<sb, 256, 0, st>>>(sc.csweeps, c->batch, prev_steps, sc.bins);
             irk::cost_scan_kernel<<<1, irk::kCostBins, 0, st>>>(sc.bins);
-            irk::cost_scatter_kernel<<<sb, 256, 0, st>>>(sc.csweeps, c->batch, chunk, sc.bins, sc.sorted);
+            irk::cost_scatter_kernel<<<sb, 256, 0, st>>>(sc.csweeps, c->batch, prev_steps, sc.bins, sc.sorted);
             irk::cost_perm_kernel<<<(unsigned)((nslots + 255) / 256), 256, 0, st>>>(sc.sorted, c->batch, nblocks, wpb,
                                                                                       spw, sc.perm);
             a.perm = sc.perm;
             a.nslots = nslots;
         }
+        prev_steps = steps;
+        c0 += steps;
         launch(a, nblocks);
         int rc = cuda_check(c, cudaGetLastError(), "ensemble kernel launch");
         if (rc) return rc;

@@ -12,7 +12,9 @@ VARIANTS = json.loads(os.environ.get("IRK_VARIANTS") or (open(_VF).read() if os.
 
 
 def build_all():
+    import shutil
     from paper_2511_03655_b200 import build
+    shutil.rmtree(os.path.join(ROOT, "paper_2511_03655_b200", "lib", "variants"), ignore_errors=True)
     for name, defs in VARIANTS.items():
         out = os.path.join(ROOT, "paper_2511_03655_b200", "lib", "variants", f"libirk_{name}.so")
         build.build(force=True, out=out, defines=tuple(defs))
