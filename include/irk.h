@@ -66,8 +66,11 @@ enum irk_option {
     IRK_OPT_BALANCE = 5,      /* ensemble scheduling: -1 = auto (default), 0 = off, C > 0 = run the
                                  call in chunks of C steps, re-sorting trajectories by the cost of
                                  the previous chunk (bitwise-neutral)  */
-    IRK_OPT_VSHARDS = 6       /* IRK_NBODY_DIRECT only: drive P body shards from this process on one
+    IRK_OPT_VSHARDS = 6,      /* IRK_NBODY_DIRECT only: drive P body shards from this process on one
                                  GPU through the sharded code path (testing the exchange layout)   */
+    IRK_OPT_LOCAL_ENERGY = 7  /* 1: track Delta H^loc_max = max_n |(H(y_n)-H(y_{n-1}))/H(y_{n-1})|
+                                 (Eq. DHlocmax) over each call, in-kernel; read it with
+                                 irk_local_energy_error (ensemble problems only)                   */
 };
 
 /* Create a context for `batch` independent trajectories of `problem` in
@@ -86,7 +89,8 @@ int irk_set_option(irk_ctx *ctx, int key, int64_t val);
 /* Bytes of caller-owned DEVICE workspace irk_integrate needs.  Layout: a
  * 64-byte header {int64 n_done, ...}, then the history L_{n-1} [8][dim][batch]
  * fp64, then per-trajectory stats [4][batch] int64 {maxiter_hits, diverged_step
- * (1-based absolute step, 0 = none), sweeps_total, reserved}, then scheduler scratch
+ * (1-based absolute step, 0 = none), sweeps_total, Delta H^loc_max of the last call
+ * (fp64 bits, IRK_OPT_LOCAL_ENERGY)}, then scheduler scratch
  * (int32 permutation and cost-sort buffers).  A zero-filled workspace means "first
  * step" (zero history, n_done = 0); reusing it continues the integration bitwise
  * as if uninterrupted (t_{n-1} = t0 + (n-1) h with the absolute n). */
@@ -115,6 +119,11 @@ int irk_energy(irk_ctx *ctx, const double *y, double *H, void *stream);
  * MAX_ITERS hits, diverged trajectories, first diverged step (-1), total sweeps}.
  * Returns IRK_E_DIVERGED, IRK_W_MAXITER or IRK_OK accordingly. */
 int irk_stats(irk_ctx *ctx, const void *workspace, void *stream, int64_t out[4]);
+
+/* After irk_integrate with IRK_OPT_LOCAL_ENERGY = 1: copy the per-trajectory
+ * Delta H^loc_max of that call (device, [batch] fp64) from the workspace to `out`
+ * (device).  Asynchronous on `stream`.  IRK_E_STATE if the option is not set. */
+int irk_local_energy_error(irk_ctx *ctx, const void *workspace, double *out, void *stream);
 
 /* Host copy of the fp64 tableau the kernels use: c~[8], b~[8], mu~[8*8], nu~[8*8]
  * (row-major [i*8+j]).  Returns IRK_OK. */

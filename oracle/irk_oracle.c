@@ -598,6 +598,9 @@ int orc_integrate(const orc_cfg *cfg, double *y, double *hist, double *energy, i
         double *hb_hist = hist + bi * (int64_t)S8 * D;
         int64_t total = 0, hits = 0, bad = -1, last = 0;
         if (energy && E > 0) energy[bi] = orc_energy(cfg->problem, D, cfg->params, cfg->nparams, yb);
+        /* Eq. DHlocmax: local relative energy error, max over this call's steps */
+        double hprev = cfg->dhloc ? orc_energy(cfg->problem, D, cfg->params, cfg->nparams, yb) : 0.0;
+        double dhmax = 0.0;
         for (int64_t n = 1; n <= cfg->nsteps; ++n) {
             if (bad >= 0) break; /* diverged trajectories are frozen */
             double tn1 = cfg->t0 + (double)(cfg->n0 + n - 1) * cfg->h; /* t_{n-1} = t0 + (n-1) h */
@@ -611,9 +614,16 @@ int orc_integrate(const orc_cfg *cfg, double *y, double *hist, double *energy, i
             if (!all_finite(yb, D)) bad = cfg->n0 + n;
             if (energy && E > 0 && n % E == 0)
                 energy[(n / E) * B + bi] = orc_energy(cfg->problem, D, cfg->params, cfg->nparams, yb);
+            if (cfg->dhloc) {
+                double hn = orc_energy(cfg->problem, D, cfg->params, cfg->nparams, yb);
+                double loc = fabs((hn - hprev) / hprev);
+                dhmax = (loc > dhmax) ? loc : dhmax;
+                hprev = hn;
+            }
         }
         for (int l = 0; l < D; ++l) y[(int64_t)l * B + bi] = yb[l];
         if (iters) iters[bi] = total;
+        if (cfg->dhloc) cfg->dhloc[bi] = dhmax;
         if (status) {
             status[3 * bi] = hits;
             status[3 * bi + 1] = bad;

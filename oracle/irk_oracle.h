@@ -38,6 +38,8 @@ typedef struct {
     const double *params;
     int nparams;
     int nthreads;          /* OpenMP threads (<=0: runtime default)                */
+    double *dhloc;         /* [batch] or NULL: max_n |(H(y_n)-H(y_{n-1}))/H(y_{n-1})| over the
+                              call's steps, Eq. DHlocmax                   */
 } orc_cfg;
 
 /* Tableau for s stages (1 <= s <= 16), rounded to fp64 exactly as DESIGN.md R-1:

@@ -49,7 +49,8 @@ class _Cfg(ctypes.Structure):
                 ("max_iters", ctypes.c_int), ("h", ctypes.c_double), ("t0", ctypes.c_double),
                 ("nsteps", ctypes.c_int64), ("batch", ctypes.c_int64), ("n0", ctypes.c_int64),
                 ("energy_every", ctypes.c_int64), ("params", ctypes.POINTER(ctypes.c_double)),
-                ("nparams", ctypes.c_int), ("nthreads", ctypes.c_int)]
+                ("nparams", ctypes.c_int), ("nthreads", ctypes.c_int),
+                ("dhloc", ctypes.POINTER(ctypes.c_double))]
 
 
 def lib():
@@ -116,12 +117,13 @@ def energy(problem: int, dim: int, params, y) -> float:
 
 def integrate(problem: int, y, params, h: float, nsteps: int, *, t0: float = 0.0, n0: int = 0,
               hist=None, mode: int = PARTITIONED, max_iters: int = 100, energy_every: int = 0,
-              nthreads: int = 0):
+              nthreads: int = 0, local_energy: bool = False):
     """Run the oracle.  y: SoA (dim, batch) (a 1-D y is one trajectory).
 
     Returns dict(y, hist, energy, iters, status) -- y in the input's shape,
     hist (batch, 8, dim), energy ((nsteps//E)+1, batch) or None, iters (batch,),
-    status (batch, 3) = {maxiter_hits, diverged_step (-1), last_step_sweeps}.
+    status (batch, 3) = {maxiter_hits, diverged_step (-1), last_step_sweeps},
+    dhloc (batch,) = max local relative energy error (Eq. DHlocmax) if local_energy.
     """
     y = _f64(y)
     one = y.ndim == 1
@@ -133,12 +135,13 @@ def integrate(problem: int, y, params, h: float, nsteps: int, *, t0: float = 0.0
     E = np.zeros(((nsteps // energy_every) + 1, batch)) if energy_every > 0 else None
     it = np.zeros(batch, dtype=np.int64)
     st = np.zeros((batch, 3), dtype=np.int64)
+    dhl = np.zeros(batch) if local_energy else None
     cfg = _Cfg(problem, dim, mode, max_iters, h, t0, nsteps, batch, n0, energy_every,
-               _dp(p), len(p), nthreads)
+               _dp(p), len(p), nthreads, _dp(dhl) if dhl is not None else None)
     rc = lib().orc_integrate(ctypes.byref(cfg), _dp(Y), _dp(H),
                              _dp(E) if E is not None else None,
                              it.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)),
                              st.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)))
     if rc:
         raise ValueError("orc_integrate: argument error")
-    return dict(y=Y[:, 0] if one else Y, hist=H, energy=E, iters=it, status=st)
+    return dict(y=Y[:, 0] if one else Y, hist=H, energy=E, iters=it, status=st, dhloc=dhl)

@@ -29,6 +29,20 @@ struct EnsArgs {
     int64_t nslots;       // launched thread slots (perm covers all of them)
     double h, t0;
     int max_iters;
+    int local_energy;     // track Delta H^loc_max (Eq. DHlocmax) into stats[3] (as double bits)
 };
+
+// running max of the local relative energy error (Eq. DHlocmax):
+// loc = |(H_n - H_{n-1}) / H_{n-1}|, NaN-ignoring max, same ops as the oracle
+__device__ __forceinline__ void dhloc_update(double hn, double &hprev, double &dmax) {
+    const double loc = fabs(__ddiv_rn(__dsub_rn(hn, hprev), hprev));
+    dmax = (loc > dmax) ? loc : dmax;
+    hprev = hn;
+}
+// combine this chunk's max with the call's running max stored in stats[3]
+__device__ __forceinline__ void dhloc_store(int64_t *stats3, bool first_chunk, double dmax) {
+    double prev = first_chunk ? 0.0 : __longlong_as_double(*stats3);
+    *stats3 = __double_as_longlong((dmax > prev) ? dmax : prev);
+}
 
 }  // namespace irk

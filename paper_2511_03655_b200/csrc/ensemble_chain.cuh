@@ -68,21 +68,29 @@ __global__ void __launch_bounds__(CH_THREADS) ens_chain_kernel(const __grid_cons
     int64_t bad = a.stats[1 * B + b];
     const int64_t n0 = *a.n_done;
     const bool sample = (a.energy != nullptr) && (a.energy_every > 0);
-    auto energy_sample = [&](int64_t idx) {
+    double hprev = 0.0, dhmax = 0.0;  // lane 0: DH^loc tracking
+    // H(y) of the chain (lane 0 sums the canonical terms); idx >= 0 stores a sample
+    auto energy_at = [&](int64_t idx, bool track) {
 #pragma unroll
         for (int s = 0; s < SPL; ++s) {
             sQV[cib][s0 + s] = q[s];
             sQV[cib][N + s0 + s] = v[s];
         }
         __syncwarp();
-        if (lane == 0) a.energy[idx * B + b] = fpu_energy<N>(sQV[cib], sQV[cib] + N, beta);
+        if (lane == 0) {
+            const double hn = fpu_energy<N>(sQV[cib], sQV[cib] + N, beta);
+            if (idx >= 0) a.energy[idx * B + b] = hn;
+            if (track) dhloc_update(hn, hprev, dhmax);
+            else hprev = hn;
+        }
         __syncwarp();
     };
-    if (sample && a.c0 == 0) energy_sample(0);
+    if ((sample && a.c0 == 0) || a.local_energy) energy_at((sample && a.c0 == 0) ? 0 : -1, false);
     if (bad > 0 || a.nsteps == 0) {
         if (lane == 0) {
             if (a.iters && a.c0 == 0) a.iters[b] = 0;
             if (a.csweeps) a.csweeps[b] = 0;
+            if (a.local_energy && a.c0 == 0) a.stats[3 * B + b] = 0;
         }
         return;
     }
@@ -196,7 +204,8 @@ __global__ void __launch_bounds__(CH_THREADS) ens_chain_kernel(const __grid_cons
             k = 0;
 #pragma unroll
             for (int s = 0; s < SPL; ++s) m[s] = p[s] = kInf;
-            if (sample && ((a.c0 + n) % a.energy_every) == 0) energy_sample((a.c0 + n) / a.energy_every);
+            const bool due = sample && ((a.c0 + n) % a.energy_every) == 0;
+            if (due || a.local_energy) energy_at(due ? (a.c0 + n) / a.energy_every : -1, a.local_energy != 0);
             if (n == a.nsteps || !finite) {
 #pragma unroll
                 for (int j = 0; j < 8; ++j)
@@ -241,6 +250,7 @@ __global__ void __launch_bounds__(CH_THREADS) ens_chain_kernel(const __grid_cons
         a.stats[2 * B + b] += sweeps;
         if (a.iters) a.iters[b] = (a.c0 == 0) ? sweeps : a.iters[b] + sweeps;
         if (a.csweeps) a.csweeps[b] = (int32_t)sweeps;
+        if (a.local_energy) dhloc_store(&a.stats[3 * B + b], a.c0 == 0, dhmax);
     }
 }
 

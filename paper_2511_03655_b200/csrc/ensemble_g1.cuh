@@ -73,7 +73,9 @@ __global__ void __maxnreg__(G1_MAXREG) ens_g1_kernel(const __grid_constant__ Ens
     const int64_t n0 = *a.n_done;
     const bool sample = (a.energy != nullptr) && (a.energy_every > 0);
     if (sample && a.c0 == 0) a.energy[b] = prob.energy(q, v);
+    double hprev = a.local_energy ? prob.energy(q, v) : 0.0, dhmax = 0.0;
     if (bad > 0 || a.nsteps == 0) {  // frozen (diverged at step `bad`, 1-based) or nothing to do
+        if (a.local_energy && a.c0 == 0) a.stats[3 * B + b] = 0;
         if (a.iters && a.c0 == 0) a.iters[b] = 0;
         if (a.csweeps) a.csweeps[b] = 0;
         return;
@@ -240,6 +242,7 @@ __global__ void __maxnreg__(G1_MAXREG) ens_g1_kernel(const __grid_constant__ Ens
             for (int l = 0; l < d; ++l) sM[l][tx] = sP[l][tx] = kInf;
             if (sample && ((a.c0 + n) % a.energy_every) == 0)
                 a.energy[((a.c0 + n) / a.energy_every) * B + b] = prob.energy(q, v);
+            if (a.local_energy) dhloc_update(prob.energy(q, v), hprev, dhmax);
             if (n == a.nsteps || !finite) {  // history = Lv (Eq. IRK_init2 extrapolates only
                                              // velocities); the q block is zeroed (R-4)
 #pragma unroll
@@ -289,6 +292,7 @@ __global__ void __maxnreg__(G1_MAXREG) ens_g1_kernel(const __grid_constant__ Ens
     a.stats[2 * B + b] += sweeps;
     if (a.iters) a.iters[b] = (a.c0 == 0) ? sweeps : a.iters[b] + sweeps;
     if (a.csweeps) a.csweeps[b] = (int32_t)sweeps;
+    if (a.local_energy) dhloc_store(&a.stats[3 * B + b], a.c0 == 0, dhmax);
 }
 
 }  // namespace irk
@@ -319,7 +323,9 @@ __global__ void __launch_bounds__(64) ens_g1fo_kernel(const __grid_constant__ En
     const int64_t n0 = *a.n_done;
     const bool sample = (a.energy != nullptr) && (a.energy_every > 0);
     if (sample && a.c0 == 0) a.energy[b] = prob.energy(y, y + d);
+    double hprev = a.local_energy ? prob.energy(y, y + d) : 0.0, dhmax = 0.0;
     if (bad > 0 || a.nsteps == 0) {
+        if (a.local_energy && a.c0 == 0) a.stats[3 * B + b] = 0;
         if (a.iters && a.c0 == 0) a.iters[b] = 0;
         if (a.csweeps) a.csweeps[b] = 0;
         return;
@@ -396,6 +402,7 @@ __global__ void __launch_bounds__(64) ens_g1fo_kernel(const __grid_constant__ En
         hits += stop ? 0 : 1;
         if (sample && ((a.c0 + n) % a.energy_every) == 0)
             a.energy[((a.c0 + n) / a.energy_every) * B + b] = prob.energy(y, y + d);
+        if (a.local_energy) dhloc_update(prob.energy(y, y + d), hprev, dhmax);
         if (!finite) {
             bad = n0 + n;
             break;
@@ -412,6 +419,7 @@ __global__ void __launch_bounds__(64) ens_g1fo_kernel(const __grid_constant__ En
     a.stats[2 * B + b] += sweeps;
     if (a.iters) a.iters[b] = (a.c0 == 0) ? sweeps : a.iters[b] + sweeps;
     if (a.csweeps) a.csweeps[b] = (int32_t)sweeps;
+    if (a.local_energy) dhloc_store(&a.stats[3 * B + b], a.c0 == 0, dhmax);
 }
 
 }  // namespace irk

@@ -111,8 +111,9 @@ __global__ void __maxnreg__(NB_MAXREG) ens_nbody_kernel(const __grid_constant__ 
     }
     const int64_t n0 = *a.n_done;
     const bool sample = (a.energy != nullptr) && (a.energy_every > 0);
-    // energy at local step 0 (first chunk only)
-    if (sample && a.c0 == 0) {
+    // energy at local step 0 (first chunk only); H(y) at the chunk start for DH^loc
+    double hprev = 0.0, dhmax = 0.0;
+    if ((sample && a.c0 == 0) || a.local_energy) {
         if (lane_ok) {
 #pragma unroll
             for (int c = 0; c < 3; ++c) {
@@ -121,7 +122,10 @@ __global__ void __maxnreg__(NB_MAXREG) ens_nbody_kernel(const __grid_constant__ 
             }
         }
         __syncwarp();
-        if (valid && body == 0) a.energy[b] = nbody_energy<NB>(sQV[gib], P);
+        if (valid && body == 0) {
+            hprev = nbody_energy<NB>(sQV[gib], P);
+            if (sample && a.c0 == 0) a.energy[b] = hprev;
+        }
         __syncwarp();
     }
     bool live = valid && bad == 0 && a.nsteps > 0;
@@ -289,8 +293,9 @@ __global__ void __maxnreg__(NB_MAXREG) ens_nbody_kernel(const __grid_constant__ 
         const unsigned nonfinite = __ballot_sync(FULL, fin && !finite);
         const bool grp_bad = fin && ((nonfinite & gmask) != 0u);
         const bool due = fin && sample && ((a.c0 + n) % a.energy_every) == 0;
-        if (__any_sync(FULL, due)) {
-            if (due) {
+        const bool need = due || (fin && a.local_energy);
+        if (__any_sync(FULL, need)) {
+            if (need) {
 #pragma unroll
                 for (int c = 0; c < 3; ++c) {
                     sQV[gib][3 * body + c] = q[c];
@@ -298,7 +303,11 @@ __global__ void __maxnreg__(NB_MAXREG) ens_nbody_kernel(const __grid_constant__ 
                 }
             }
             __syncwarp();
-            if (due && body == 0) a.energy[((a.c0 + n) / a.energy_every) * B + b] = nbody_energy<NB>(sQV[gib], P);
+            if (need && body == 0) {
+                const double hn = nbody_energy<NB>(sQV[gib], P);
+                if (due) a.energy[((a.c0 + n) / a.energy_every) * B + b] = hn;
+                if (a.local_energy) dhloc_update(hn, hprev, dhmax);
+            }
             __syncwarp();
         }
         if (fin && (n == a.nsteps || grp_bad)) {  // leave: history = Lv (R-4), q block zeroed
@@ -352,6 +361,9 @@ __global__ void __maxnreg__(NB_MAXREG) ens_nbody_kernel(const __grid_constant__ 
                 a.stats[2 * B + b] += sweeps;
                 if (a.iters) a.iters[b] = (a.c0 == 0) ? sweeps : a.iters[b] + sweeps;
                 if (a.csweeps) a.csweeps[b] = (int32_t)sweeps;
+                if (a.local_energy) dhloc_store(&a.stats[3 * B + b], a.c0 == 0, dhmax);
+            } else if (a.local_energy && a.c0 == 0) {
+                a.stats[3 * B + b] = 0;
             }
         }
     }

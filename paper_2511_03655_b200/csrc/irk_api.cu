@@ -31,6 +31,7 @@ struct irk_ctx {
     bool have_params = false;
     int mode = 0, max_iters = 100, mapping = 0;
     int64_t balance = -1;  // IRK_OPT_BALANCE: -1 auto, 0 off, >0 chunk length
+    int local_energy = 0;  // IRK_OPT_LOCAL_ENERGY
     int64_t energy_every = 0;
     Tableau T;
     std::string err;
@@ -327,6 +328,7 @@ EnsArgs ens_args(irk_ctx *c, double *y, double t0, char *ws, double *energy, int
     a.h = c->h;
     a.t0 = t0;
     a.max_iters = c->max_iters;
+    a.local_energy = c->local_energy;
     return a;
 }
 
@@ -567,6 +569,12 @@ int irk_set_option(irk_ctx *c, int key, int64_t val) {
         if (val < -1) return fail(c, IRK_E_ARG, "irk_set_option: bad BALANCE");
         c->balance = val;
         return IRK_OK;
+    case IRK_OPT_LOCAL_ENERGY:
+        if (val != 0 && val != 1) return fail(c, IRK_E_ARG, "irk_set_option: LOCAL_ENERGY must be 0 or 1");
+        if (val && c->problem == IRK_NBODY_DIRECT)
+            return fail(c, IRK_E_ARG, "irk_set_option: LOCAL_ENERGY is for the ensemble problems (use ENERGY_EVERY)");
+        c->local_energy = (int)val;
+        return IRK_OK;
     case IRK_OPT_VSHARDS:
         if (c->problem != IRK_NBODY_DIRECT || val < 1 || (c->dim / 6) % val || c->nccl_comm)
             return fail(c, IRK_E_ARG, "irk_set_option: VSHARDS needs IRK_NBODY_DIRECT, N %% P == 0, no NCCL comm");
@@ -764,6 +772,15 @@ int irk_stats(irk_ctx *c, const void *workspace, void *stream, int64_t out[4]) {
     if (div_traj) return IRK_E_DIVERGED;
     if (hit_traj) return IRK_W_MAXITER;
     return IRK_OK;
+}
+
+int irk_local_energy_error(irk_ctx *c, const void *workspace, double *out, void *stream) {
+    if (!c || !workspace || !out) return IRK_E_ARG;
+    if (!c->local_energy) return fail(c, IRK_E_STATE, "irk_local_energy_error: IRK_OPT_LOCAL_ENERGY not set");
+    const char *src = static_cast<const char *>(workspace) + kHeader + hist_bytes(c) + sizeof(int64_t) * 3 * c->batch;
+    return cuda_check(c, cudaMemcpyAsync(out, src, sizeof(double) * c->batch, cudaMemcpyDeviceToDevice,
+                                         reinterpret_cast<cudaStream_t>(stream)),
+                      "D2D dhloc");
 }
 
 int irk_tableau(double *c, double *b, double *mu, double *nu) {

@@ -15,6 +15,7 @@ import numpy as np
 KEPLER, NBODY, FPU_BETA, HENON_HEILES, NBODY_DIRECT = 1, 2, 3, 4, 5
 OK, W_MAXITER, E_ARG, E_CUDA, E_DIVERGED, E_COMM, E_STATE = 0, 1, -1, -2, -3, -4, -5
 OPT_MODE, OPT_MAX_ITERS, OPT_ENERGY_EVERY, OPT_MAPPING, OPT_BALANCE, OPT_VSHARDS = 1, 2, 3, 4, 5, 6
+OPT_LOCAL_ENERGY = 7
 PARTITIONED, FIRST_ORDER = 0, 1
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
@@ -23,7 +24,7 @@ LIB_PATH = os.environ.get("IRK_LIB_OVERRIDE") or os.path.join(_HERE, "lib", "lib
 SYMBOLS = ["irk_create", "irk_set_params", "irk_set_option", "irk_workspace_bytes",
            "irk_integrate", "irk_integrate_host", "irk_energy", "irk_stats", "irk_tableau",
            "irk_set_comm", "irk_nccl_unique_id", "irk_last_error", "irk_destroy", "irk_probe_dfma",
-           "irk_probe_divsqrt"]
+           "irk_probe_divsqrt", "irk_local_energy_error"]
 
 _lib = None
 _lock = threading.Lock()
@@ -64,6 +65,7 @@ def lib():
             l.irk_probe_dfma.argtypes = [vp, ctypes.c_int, ctypes.c_int, vp]
             l.irk_probe_dfma.restype = ctypes.c_int64
             l.irk_probe_divsqrt.argtypes = [vp, vp, vp, ctypes.c_int64, vp]
+            l.irk_local_energy_error.argtypes = [vp, vp, vp, vp]
             _lib = l
     return _lib
 
@@ -90,7 +92,7 @@ class Integrator:
 
     def __init__(self, problem: int, dim: int, h: float, nsteps: int, batch: int, params,
                  *, mode: int = PARTITIONED, max_iters: int = 100, energy_every: int = 0,
-                 mapping: int = 0, balance: int = -1, vshards: int = 1):
+                 mapping: int = 0, balance: int = -1, vshards: int = 1, local_energy: bool = False):
         L = lib()
         self._ctx = L.irk_create(problem, dim, h, nsteps, batch)
         if not self._ctx:
@@ -105,6 +107,8 @@ class Integrator:
             self._check(L.irk_set_option(self._ctx, key, val))
         if vshards != 1:
             self._check(L.irk_set_option(self._ctx, OPT_VSHARDS, vshards))
+        if local_energy:
+            self._check(L.irk_set_option(self._ctx, OPT_LOCAL_ENERGY, 1))
         self.rank, self.nranks = 0, 1
 
     def set_comm(self, unique_id: bytes, rank: int, nranks: int):
@@ -189,6 +193,15 @@ class Integrator:
             self._check(rc)
         return rc, dict(maxiter_traj=int(out[0]), diverged_traj=int(out[1]),
                         first_bad_step=int(out[2]), total_sweeps=int(out[3]))
+
+    def local_energy_error(self, workspace, stream=None):
+        """Per-trajectory Delta H^loc_max of the last call (IRK_OPT_LOCAL_ENERGY)."""
+        import torch
+        out = torch.empty(self.batch, dtype=torch.float64, device=workspace.device)
+        s = torch.cuda.current_stream(workspace.device) if stream is None else stream
+        self._check(lib().irk_local_energy_error(self._ctx, _ptr(workspace), _ptr(out),
+                                                 ctypes.c_void_p(s.cuda_stream)))
+        return out
 
     def hist_view(self, workspace):
         """The history block of a workspace as a float64 (8, dim, batch) tensor view."""

@@ -413,3 +413,37 @@ def test_config5_nccl_single_rank_path(irk, orc):
         assert np.array_equal(Y.cpu().numpy(), o["y"])
         assert np.array_equal(E.cpu().numpy(), o["energy"])
         assert H[0] == orc.energy(w.problem, w.dim, w.params, o["y"][:, 0])
+
+
+# ------------------------------------------------- local energy error (f2)
+@pytest.mark.parametrize("which", ["kepler", "hh", "hh_fo", "nbody", "fpu"])
+def test_local_energy_error_parity(irk, orc, which):
+    """In-kernel Delta H^loc_max (Eq. DHlocmax, IRK_OPT_LOCAL_ENERGY) equals the
+    oracle's bit for bit, also across chunked calls and balance chunks."""
+    mode = 0
+    if which == "kepler":
+        w = wl.kepler_ensemble(batch=9000, nsteps=400)
+    elif which == "hh":
+        w = wl.henon_heiles(batch=100, nsteps=400)
+    elif which == "hh_fo":
+        w = wl.henon_heiles(batch=50, nsteps=300, h=0.05)
+        mode = 1
+    elif which == "nbody":
+        w = wl.six_body_ensemble(batch=12, nsteps=300)
+    else:
+        w = wl.fpu_ensemble(batch=6, nsteps=300)
+    with irk.Integrator(w.problem, w.dim, w.h, w.nsteps // 2, w.batch, w.params, mode=mode,
+                        local_energy=True) as ig:
+        Y = torch.tensor(w.y, dtype=torch.float64, device="cuda")
+        ws = ig.new_workspace()
+        ig.integrate(Y, ws)
+        d1 = ig.local_energy_error(ws).cpu().numpy()
+        y1 = Y.cpu().numpy()
+        ig.integrate(Y, ws)
+        d2 = ig.local_energy_error(ws).cpu().numpy()
+    o1 = orc.integrate(w.problem, w.y, w.params, w.h, w.nsteps // 2, mode=mode, local_energy=True)
+    o2 = orc.integrate(w.problem, o1["y"], w.params, w.h, w.nsteps // 2, mode=mode, local_energy=True,
+                       n0=w.nsteps // 2, hist=o1["hist"])
+    assert np.array_equal(y1, o1["y"])
+    assert np.array_equal(d1, o1["dhloc"]) and np.array_equal(d2, o2["dhloc"])
+    assert np.all(d1 > 0)

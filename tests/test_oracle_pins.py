@@ -363,3 +363,31 @@ def test_argument_errors(orc):
         orc.integrate(wl.KEPLER, np.zeros(4), [1.0], 0.0, 1)
     with pytest.raises(ValueError):
         orc.integrate(wl.NBODY_DIRECT, np.zeros(12), [1.0, 0.0, 1.0, 1.0], 0.1, 1)
+
+
+def test_local_energy_error_pins(orc):
+    """Eq. DHlocmax: for the harmonic oscillator the Gauss solution
+    conserves the quadratic energy exactly, so Delta H^loc_max is roundoff
+    (<= 4 ulp); for Henon-Heiles at the paper's h = 2 pi/68 it is at
+    roundoff level too, while a coarse h shows the truncation error."""
+    y0 = np.array([0.3, -0.7, 0.5, 0.2])
+    r = orc.integrate(wl.HENON_HEILES, y0, [0.0, 0.0], 2 * math.pi / 8, 400, local_energy=True)
+    assert r["dhloc"][0] <= 4 * EPS
+    w = wl.henon_heiles(nsteps=2000)
+    r = orc.integrate(w.problem, w.y, w.params, w.h, w.nsteps, local_energy=True)
+    assert r["dhloc"][0] < 5e-15
+    e = r["energy"] if r["energy"] is not None else None
+    r2 = orc.integrate(w.problem, w.y, w.params, 2 * math.pi / 6, 200, local_energy=True)
+    assert r2["dhloc"][0] > 1e-8
+    # the value is the max over steps of |(H_n - H_{n-1}) / H_{n-1}| (checked step by step)
+    y = w.y[:, 0].copy()
+    hmax = 0.0
+    hist = None
+    for n in range(50):
+        rr = orc.integrate(w.problem, y, w.params, w.h, 1, n0=n, hist=hist)
+        h0 = orc.energy(w.problem, 4, w.params, y)
+        h1 = orc.energy(w.problem, 4, w.params, rr["y"])
+        hmax = max(hmax, abs((h1 - h0) / h0))
+        y, hist = rr["y"], rr["hist"]
+    r3 = orc.integrate(w.problem, w.y, w.params, w.h, 50, local_energy=True)
+    assert r3["dhloc"][0] == hmax
