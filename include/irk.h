@@ -68,6 +68,11 @@ enum irk_option {
                                  the previous chunk (bitwise-neutral)  */
     IRK_OPT_VSHARDS = 6,      /* IRK_NBODY_DIRECT only: drive P body shards from this process on one
                                  GPU through the sharded code path (testing the exchange layout)   */
+    IRK_OPT_SCHEDULE = 8,     /* ensemble launch: 0 = auto (default), 1 = chunked launches with the
+                                 cost sort of BALANCE, 2 = one persistent launch whose lanes pull
+                                 (trajectory, step-chunk) units from a work queue (per-thread
+                                 problems, partitioned mode; BALANCE = C > 0 sets the unit length).
+                                 Bitwise-neutral                          */
     IRK_OPT_LOCAL_ENERGY = 7  /* 1: track Delta H^loc_max = max_n |(H(y_n)-H(y_{n-1}))/H(y_{n-1})|
                                  (Eq. DHlocmax) over each call, in-kernel; read it with
                                  irk_local_energy_error (ensemble problems only)                   */
@@ -78,7 +83,7 @@ enum irk_option {
  * irk_integrate call.  Builds the tableau in __float128 (Newton on P_8,
  * Bjorck-Pereyra Vandermonde solves), checks B(16), C(8), the symplectic
  * condition and the mu~ identity, and rounds it (R-1).  Returns NULL
- * on error (message via irk_last_error(NULL)). */
+ * on error (message via irk_last_error(NULL)); 1 <= batch <= 2^31 - 1. */
 irk_ctx *irk_create(int problem, int dim, double h, int64_t nsteps, int64_t batch);
 
 /* Copy n host doubles of problem parameters (see enum irk_problem). */

@@ -39,9 +39,19 @@ __device__ __forceinline__ void dhloc_update(double hn, double &hprev, double &d
     dmax = (loc > dmax) ? loc : dmax;
     hprev = hn;
 }
+// inter-unit hand-off of the work-queue kernels (gpu-scope release / acquire)
+__device__ __forceinline__ int32_t ld_acquire(const int32_t *p) {
+    int32_t v;
+    asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release(int32_t *p, int32_t v) {
+    asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
 // combine this chunk's max with the call's running max stored in stats[3]
 __device__ __forceinline__ void dhloc_store(int64_t *stats3, bool first_chunk, double dmax) {
-    double prev = first_chunk ? 0.0 : __longlong_as_double(*stats3);
+    double prev = first_chunk ? 0.0 : __longlong_as_double(__ldcg(stats3));
     *stats3 = __double_as_longlong((dmax > prev) ? dmax : prev);
 }
 

@@ -299,6 +299,270 @@ __global__ void __maxnreg__(G1_MAXREG) ens_g1_kernel(const __grid_constant__ Ens
 
 namespace irk {
 
+// ---------------------------------------------------------------------------
+// ens_g1q: the g1 mapping as ONE persistent launch with a per-lane work queue.
+//
+// The chunked ens_g1 launches B threads per chunk; at 168 registers a B200 holds
+// 148 x 384 = 56,832 of them, so config 2 (B = 65,536) runs 1.15 waves and the
+// partial wave idles most of the GPU (ncu, profiles/r1: 87% of cycles active).
+// Here the grid is exactly the resident capacity and every lane pulls work
+// units u = c*B + b (trajectory b, step chunk c of `qchunk` steps) from a global
+// counter; a lane that finishes a unit stores (y, history, stats), publishes
+// progress[b] = c + 1 and pulls the next unit in the same sweep-granular loop,
+// so lanes stay busy until the queue drains (tail <= one unit).  Unit (b, c)
+// waits (idle trips) until unit (b, c-1) is published; it was issued B units
+// earlier, so this is rare.  Each unit does exactly the arithmetic of the
+// corresponding chunk of ens_g1 (same nu-init from the stored history, same
+// absolute step index), so results are bitwise those of any other schedule.
+//
+// The stop test's comparisons run on the integer pipe: every operand is a
+// non-negative, non-NaN double (|.|, NaN mapped to 0 as the canonical
+// NaN-ignoring max does, +inf for "no history"), whose IEEE order is the order
+// of the bit patterns as int64.
+struct QueueArgs {
+    unsigned long long *counter;  // next unit
+    int32_t *progress;            // [batch] chunks completed in this call
+    int64_t qchunk;               // steps per unit
+    int64_t nchunks;              // units per trajectory
+};
+
+__device__ __forceinline__ int64_t dbits(double x) { return __double_as_longlong(x); }
+// |a - b| as bits, NaN -> 0 (the NaN-ignoring max never selects a NaN)
+__device__ __forceinline__ int64_t absdiff_bits(double a, double b) {
+    const int64_t e = dbits(dsub(a, b)) & 0x7fffffffffffffffLL;
+    return (e > 0x7ff0000000000000LL) ? 0 : e;
+}
+__device__ __forceinline__ int64_t imax64(int64_t a, int64_t b) { return a > b ? a : b; }
+__device__ __forceinline__ int64_t imin64(int64_t a, int64_t b) { return a < b ? a : b; }
+
+template <class P>
+__global__ void __maxnreg__(G1_MAXREG) ens_g1q_kernel(const __grid_constant__ EnsArgs a,
+                                                     const __grid_constant__ QueueArgs qa,
+                                                     const __grid_constant__ P prob) {
+    constexpr int d = P::d, D = 2 * d;
+    const int64_t B = a.batch;
+    __shared__ __align__(16) double sW[2][64];  // [0] = mu~, [1] = nu~ (row-major)
+    for (int e = threadIdx.x; e < 128; e += blockDim.x) sW[e >> 6][e & 63] = (e < 64) ? (&c_mu[0][0])[e] : (&c_nu[0][0])[e - 64];
+    __syncthreads();
+    __shared__ double sQ[8 * d][G1_THREADS], sL[8 * d][G1_THREADS];
+    __shared__ int64_t sM[d][G1_THREADS], sP[d][G1_THREADS];
+    const int tx = threadIdx.x;
+    const int64_t n0 = *a.n_done;
+    const bool sample = (a.energy != nullptr) && (a.energy_every > 0);
+    const int64_t total = B * qa.nchunks;
+    const int64_t kInfBits = 0x7ff0000000000000LL;
+
+    double q[d], v[d], V[8][d];
+    int32_t b = -1;  // trajectory of the held unit (-1: none)
+    int64_t c = 0, len = 0, n = 0, hits = 0, sweeps = 0, u = -1;
+    double hprev = 0.0, dhmax = 0.0;
+    int k = 0;
+    for (;;) {
+        if (b < 0) {  // ---- acquire the next unit (divergent, once per unit) ----
+            if (u < 0) u = (int64_t)atomicAdd(qa.counter, 1ull);
+            if (u >= total) break;
+            c = u / B;
+            const int32_t bb = (int32_t)(u - c * B);
+            if (c > 0 && ld_acquire(&qa.progress[bb]) < c) {  // predecessor unit still running
+                __nanosleep(256);
+                continue;
+            }
+            u = -1;
+            b = bb;
+            const int64_t c0 = c * qa.qchunk;
+            len = (a.nsteps - c0 < qa.qchunk) ? a.nsteps - c0 : qa.qchunk;
+#pragma unroll
+            for (int l = 0; l < d; ++l) {
+                q[l] = __ldcg(&a.y[l * B + b]);  // L2: written by another SM's unit
+                v[l] = __ldcg(&a.y[(d + l) * B + b]);
+            }
+            if (sample && c == 0) a.energy[b] = prob.energy(q, v);
+            hprev = a.local_energy ? prob.energy(q, v) : 0.0;
+            dhmax = 0.0;
+            if (__ldcg(&a.stats[1 * B + b]) > 0 || len <= 0) {  // frozen (diverged earlier): nothing to do
+                if (c == 0) {
+                    if (a.local_energy) a.stats[3 * B + b] = 0;
+                    if (a.iters) a.iters[b] = 0;
+                }
+                st_release(&qa.progress[b], (int32_t)(c + 1));
+                b = -1;
+                continue;
+            }
+            {   // a1: nu-init from the history (zeros = first step of the run)
+                double H[8][d];
+#pragma unroll
+                for (int j = 0; j < 8; ++j)
+#pragma unroll
+                    for (int l = 0; l < d; ++l) H[j][l] = __ldcg(&a.hist[((int64_t)j * D + d + l) * B + b]);
+#pragma unroll
+                for (int i = 0; i < 8; ++i)
+#pragma unroll
+                    for (int l = 0; l < d; ++l) {
+                        double acc = dmul(c_nu[i][0], H[0][l]);
+#pragma unroll
+                        for (int j = 1; j < 8; ++j) acc = dfma(c_nu[i][j], H[j][l], acc);
+                        V[i][l] = dadd(v[l], acc);
+                    }
+            }
+#pragma unroll
+            for (int l = 0; l < d; ++l) sM[l][tx] = sP[l][tx] = kInfBits;
+            n = hits = sweeps = 0;
+            k = 0;
+        }
+        ++k;
+        // a2: Lq_j = hb_j V_j ; Q_i^[k] = q + D(mu_i., Lq)  (+ a5 on the fly)
+        double Lq[8][d], sLq[d];
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+#pragma unroll
+            for (int l = 0; l < d; ++l) Lq[j][l] = dmul(a.hb[j], V[j][l]);
+#pragma unroll
+        for (int l = 0; l < d; ++l) {
+            sLq[l] = Lq[0][l];
+#pragma unroll
+            for (int j = 1; j < 8; ++j) sLq[l] = dadd(sLq[l], Lq[j][l]);
+        }
+        bool stop = (k >= 2);
+        int64_t delta[d];
+        {
+            int64_t ev[d][8];
+            const double2 *M = reinterpret_cast<const double2 *>(&c_mu[0][0]);
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                double2 w[4];
+#pragma unroll
+                for (int jj = 0; jj < 4; ++jj) w[jj] = M[i * 4 + jj];
+#pragma unroll
+                for (int l = 0; l < d; ++l) {
+                    double acc = dmul(w[0].x, Lq[0][l]);
+                    acc = dfma(w[0].y, Lq[1][l], acc);
+#pragma unroll
+                    for (int jj = 1; jj < 4; ++jj) {
+                        acc = dfma(w[jj].x, Lq[2 * jj][l], acc);
+                        acc = dfma(w[jj].y, Lq[2 * jj + 1][l], acc);
+                    }
+                    const double qn = dadd(q[l], acc);
+                    ev[l][i] = absdiff_bits(qn, sQ[i * d + l][tx]);  // garbage at k = 1, unused
+                    sQ[i * d + l][tx] = qn;
+                }
+            }
+#pragma unroll
+            for (int l = 0; l < d; ++l)
+                delta[l] = imax64(imax64(imax64(ev[l][0], ev[l][1]), imax64(ev[l][2], ev[l][3])),
+                                  imax64(imax64(ev[l][4], ev[l][5]), imax64(ev[l][6], ev[l][7])));
+        }
+        if (k >= 2) {  // a5, reading R2 (Delta^[k] exists from k = 2), on the bit patterns
+#pragma unroll
+            for (int l = 0; l < d; ++l) {
+                const int64_t pl = sP[l][tx], ml = sM[l][tx];
+                const bool ok = (delta[l] == 0) || (ml <= imin64(delta[l], pl));
+                sM[l][tx] = imin64(pl, ml);
+                sP[l][tx] = delta[l];
+                stop = stop && ok;
+            }
+        }
+        // a3 + a4 (first half): F_i = g(Q_i, t_i) ; Lv_i = hb_i F_i, all eight stages in flight
+        const int64_t nabs = n0 + c * qa.qchunk + n;  // absolute index of the step being taken
+        const double tn1 = dadd(a.t0, dmul((double)nabs, a.h));
+        double Lv[8][d];
+        {
+            bool ok = true;
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                double Qi[d];
+#pragma unroll
+                for (int l = 0; l < d; ++l) Qi[l] = sQ[i * d + l][tx];
+                prob.template accel<false>(Qi, Lv[i], dadd(tn1, dmul(c_c[i], a.h)), ok);
+            }
+            if (!ok) {  // some stage needs the exact slow path of div/sqrt: redo all, same bits
+#pragma unroll 1
+                for (int i = 0; i < 8; ++i) {
+                    double Qi[d], Fi[d];
+#pragma unroll
+                    for (int l = 0; l < d; ++l) Qi[l] = sQ[i * d + l][tx];
+                    prob.template accel<true>(Qi, Fi, dadd(tn1, dmul(c_c[i], a.h)), ok);
+#pragma unroll
+                    for (int l = 0; l < d; ++l) sL[i * d + l][tx] = Fi[l];
+                }
+#pragma unroll
+                for (int i = 0; i < 8; ++i)
+#pragma unroll
+                    for (int l = 0; l < d; ++l) Lv[i][l] = sL[i * d + l][tx];
+            }
+#pragma unroll
+            for (int i = 0; i < 8; ++i)
+#pragma unroll
+                for (int l = 0; l < d; ++l) Lv[i][l] = dmul(a.hb[i], Lv[i][l]);
+        }
+        const bool fin = stop || (k >= a.max_iters);
+        if (fin) {  // a6: update with the last iteration's L, history <- Lv
+            bool finite = true;
+#pragma unroll
+            for (int l = 0; l < d; ++l) {
+                double sv = Lv[0][l];
+#pragma unroll
+                for (int j = 1; j < 8; ++j) sv = dadd(sv, Lv[j][l]);
+                q[l] = dadd(q[l], sLq[l]);
+                v[l] = dadd(v[l], sv);
+                finite = finite && isfinite(q[l]) && isfinite(v[l]);
+            }
+            ++n;
+            sweeps += k;
+            hits += stop ? 0 : 1;
+            k = 0;
+#pragma unroll
+            for (int l = 0; l < d; ++l) sM[l][tx] = sP[l][tx] = kInfBits;
+            const int64_t nloc = c * qa.qchunk + n;  // call-local step index just completed
+            if (sample && (nloc % a.energy_every) == 0)
+                a.energy[(nloc / a.energy_every) * B + b] = prob.energy(q, v);
+            if (a.local_energy) dhloc_update(prob.energy(q, v), hprev, dhmax);
+            if (n == len || !finite) {  // ---- release the unit ----
+#pragma unroll
+                for (int j = 0; j < 8; ++j)
+#pragma unroll
+                    for (int l = 0; l < d; ++l) {
+                        a.hist[((int64_t)j * D + l) * B + b] = 0.0;
+                        a.hist[((int64_t)j * D + d + l) * B + b] = Lv[j][l];
+                    }
+#pragma unroll
+                for (int l = 0; l < d; ++l) {
+                    a.y[l * B + b] = q[l];
+                    a.y[(d + l) * B + b] = v[l];
+                }
+                a.stats[0 * B + b] = __ldcg(&a.stats[0 * B + b]) + hits;
+                if (!finite) a.stats[1 * B + b] = n0 + nloc;
+                a.stats[2 * B + b] = __ldcg(&a.stats[2 * B + b]) + sweeps;
+                if (a.iters) a.iters[b] = (c == 0) ? sweeps : __ldcg(&a.iters[b]) + sweeps;
+                if (a.local_energy) dhloc_store(&a.stats[3 * B + b], c == 0, dhmax);
+                st_release(&qa.progress[b], (int32_t)(c + 1));
+                b = -1;
+                continue;
+            }
+        }
+        // a4 (second half) / next step's a1: V_i = v + D(W_i., Lv), W = fin ? nu : mu
+        {
+            const double2 *W = reinterpret_cast<const double2 *>(&sW[fin ? 1 : 0][0]);
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                double2 w[4];
+#pragma unroll
+                for (int jj = 0; jj < 4; ++jj) w[jj] = W[i * 4 + jj];
+#pragma unroll
+                for (int l = 0; l < d; ++l) {
+                    double acc = dmul(w[0].x, Lv[0][l]);
+                    acc = dfma(w[0].y, Lv[1][l], acc);
+#pragma unroll
+                    for (int jj = 1; jj < 4; ++jj) {
+                        acc = dfma(w[jj].x, Lv[2 * jj][l], acc);
+                        acc = dfma(w[jj].y, Lv[2 * jj + 1][l], acc);
+                    }
+                    V[i][l] = dadd(v[l], acc);
+                }
+            }
+        }
+    }
+}
+
 // First-order mode (Eqs. IRK_init / IRK_FP) for the per-thread
 // problems: all D = 2d components are extrapolated (a1 over y), each sweep
 // evaluates F_i = (V-part of Y_i, g(Q-part of Y_i, t_i)), L = hb o F,

@@ -31,6 +31,8 @@ struct irk_ctx {
     bool have_params = false;
     int mode = 0, max_iters = 100, mapping = 0;
     int64_t balance = -1;  // IRK_OPT_BALANCE: -1 auto, 0 off, >0 chunk length
+    int schedule = 0;      // IRK_OPT_SCHEDULE: 0 auto, 1 chunked launches, 2 persistent work queue
+    int g1q_blocks_per_sm = 0;  // occupancy of ens_g1q (queried once)
     int local_energy = 0;  // IRK_OPT_LOCAL_ENERGY
     int64_t energy_every = 0;
     Tableau T;
@@ -332,11 +334,52 @@ EnsArgs ens_args(irk_ctx *c, double *y, double t0, char *ws, double *energy, int
     return a;
 }
 
+// Persistent work-queue launch of the g1 mapping (ensemble_g1.cuh, ens_g1q):
+// grid = resident capacity, units of `qchunk` steps per trajectory.
+template <class P>
+int launch_g1q(irk_ctx *c, const P &prob, EnsArgs &a, char *ws, cudaStream_t st) {
+    int rc;
+    if (!c->g1q_blocks_per_sm &&
+        (rc = cuda_check(c, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c->g1q_blocks_per_sm, irk::ens_g1q_kernel<P>,
+                                                                           irk::G1_THREADS, 0),
+                         "occupancy")))
+        return rc;
+    int dev = 0, sms = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int64_t lanes = (int64_t)sms * (c->g1q_blocks_per_sm > 0 ? c->g1q_blocks_per_sm : 1) * irk::G1_THREADS;
+    const int64_t need = (c->batch + irk::G1_THREADS - 1) / irk::G1_THREADS;
+    const int64_t blocks = need < lanes / irk::G1_THREADS ? need : lanes / irk::G1_THREADS;
+    irk::QueueArgs qa;
+    Sched sc = sched_of(c, ws);
+    qa.progress = sc.perm;
+    qa.counter = reinterpret_cast<unsigned long long *>(sc.bins);
+    // one unit per trajectory when every trajectory has its own lane; else ~32 units each
+    int64_t chunk = c->nsteps;
+    if (c->balance > 0) chunk = c->balance;
+    else if (c->balance < 0 && c->batch > lanes) chunk = (c->nsteps + 31) / 32;
+    if (chunk < 1) chunk = 1;
+    qa.qchunk = chunk;
+    qa.nchunks = c->nsteps > 0 ? (c->nsteps + chunk - 1) / chunk : 1;
+    a.nsteps = c->nsteps;
+    a.c0 = 0;
+    a.csweeps = nullptr;
+    a.perm = nullptr;
+    a.nslots = c->batch;
+    if ((rc = cuda_check(c, cudaMemsetAsync(sc.perm, 0, sizeof(int32_t) * c->batch, st), "memset progress"))) return rc;
+    if ((rc = cuda_check(c, cudaMemsetAsync(sc.bins, 0, sizeof(unsigned long long), st), "memset counter"))) return rc;
+    irk::ens_g1q_kernel<P><<<(unsigned)blocks, irk::G1_THREADS, 0, st>>>(a, qa, prob);
+    if ((rc = cuda_check(c, cudaGetLastError(), "ens_g1q launch"))) return rc;
+    advance_n_kernel<<<1, 1, 0, st>>>(reinterpret_cast<int64_t *>(ws), c->nsteps);
+    return cuda_check(c, cudaGetLastError(), "advance_n launch");
+}
+
 template <class P>
 int launch_g1(irk_ctx *c, const P &prob, double *y, double t0, char *ws, double *energy,
               int64_t *iters, cudaStream_t st) {
     EnsArgs a = ens_args(c, y, t0, ws, energy, iters);
     const int64_t blocks = (c->batch + irk::G1_THREADS - 1) / irk::G1_THREADS;
+    if (c->mode == 0 && c->schedule != 1) return launch_g1q(c, prob, a, ws, st);
     if (c->mode == 1)
         return run_chunks(c, a, ws, blocks, irk::G1_THREADS / 32, 32, st, [&](const EnsArgs &aa, int64_t nb) {
             irk::ens_g1fo_kernel<P><<<(unsigned)nb, irk::G1_THREADS, 0, st>>>(aa, prob);
@@ -520,6 +563,7 @@ irk_ctx *irk_create(int problem, int dim, double h, int64_t nsteps, int64_t batc
     if (!std::isfinite(h) || h == 0.0) return bad("irk_create: h must be finite and nonzero");
     if (nsteps < 0) return bad("irk_create: nsteps < 0");
     if (batch < 1) return bad("irk_create: batch < 1");
+    if (batch > 0x7fffffffLL) return bad("irk_create: batch > 2^31 - 1 (int32 trajectory indices)");
     irk_ctx *c = new irk_ctx;
     c->problem = problem;
     c->dim = dim;
@@ -579,6 +623,10 @@ int irk_set_option(irk_ctx *c, int key, int64_t val) {
         if (c->problem != IRK_NBODY_DIRECT || val < 1 || (c->dim / 6) % val || c->nccl_comm)
             return fail(c, IRK_E_ARG, "irk_set_option: VSHARDS needs IRK_NBODY_DIRECT, N %% P == 0, no NCCL comm");
         c->vshards = (int)val;
+        return IRK_OK;
+    case IRK_OPT_SCHEDULE:
+        if (val < 0 || val > 2) return fail(c, IRK_E_ARG, "irk_set_option: SCHEDULE must be 0, 1 or 2");
+        c->schedule = (int)val;
         return IRK_OK;
     case IRK_OPT_MAPPING:
         if (val < 0 || val > 1) return fail(c, IRK_E_ARG, "irk_set_option: MAPPING must be 0 (auto) or 1");

@@ -16,6 +16,7 @@ KEPLER, NBODY, FPU_BETA, HENON_HEILES, NBODY_DIRECT = 1, 2, 3, 4, 5
 OK, W_MAXITER, E_ARG, E_CUDA, E_DIVERGED, E_COMM, E_STATE = 0, 1, -1, -2, -3, -4, -5
 OPT_MODE, OPT_MAX_ITERS, OPT_ENERGY_EVERY, OPT_MAPPING, OPT_BALANCE, OPT_VSHARDS = 1, 2, 3, 4, 5, 6
 OPT_LOCAL_ENERGY = 7
+OPT_SCHEDULE = 8
 PARTITIONED, FIRST_ORDER = 0, 1
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
@@ -92,7 +93,8 @@ class Integrator:
 
     def __init__(self, problem: int, dim: int, h: float, nsteps: int, batch: int, params,
                  *, mode: int = PARTITIONED, max_iters: int = 100, energy_every: int = 0,
-                 mapping: int = 0, balance: int = -1, vshards: int = 1, local_energy: bool = False):
+                 mapping: int = 0, balance: int = -1, vshards: int = 1, local_energy: bool = False,
+                 schedule: int = 0):
         L = lib()
         self._ctx = L.irk_create(problem, dim, h, nsteps, batch)
         if not self._ctx:
@@ -103,7 +105,7 @@ class Integrator:
         self._check(L.irk_set_params(self._ctx, _dp(p), len(p)))
         for key, val in ((OPT_MODE, mode), (OPT_MAX_ITERS, max_iters),
                          (OPT_ENERGY_EVERY, energy_every), (OPT_MAPPING, mapping),
-                         (OPT_BALANCE, balance)):
+                         (OPT_BALANCE, balance), (OPT_SCHEDULE, schedule)):
             self._check(L.irk_set_option(self._ctx, key, val))
         if vshards != 1:
             self._check(L.irk_set_option(self._ctx, OPT_VSHARDS, vshards))

@@ -235,6 +235,42 @@ def test_cost_balanced_schedule_is_bitwise_neutral(irk, orc):
     assert np.array_equal(outs[1][2][idx], orr["iters"])
 
 
+def test_work_queue_schedule_bitwise(irk, orc):
+    """The persistent work-queue launch (IRK_OPT_SCHEDULE = 2): more trajectories
+    than resident lanes, 17 units of 7 steps per trajectory (hand-offs between
+    lanes and SMs), energy samples and Delta H^loc straddling units, and two
+    trajectories that diverge mid-call.  Bitwise equal to the chunked launches
+    and to the oracle on a sample that includes the diverged trajectories."""
+    w = wl.kepler_ensemble(batch=70001, nsteps=119)
+    y = w.y.copy()
+    y[:, 5] = [1e-200, 0.0, 0.0, 0.0]      # r = 0 -> non-finite at step 1
+    y[:, 69990] = [1e-150, 0.0, 0.0, 1e-160]
+    outs = []
+    for sched, bal in ((1, 0), (2, 7), (0, -1)):
+        with irk.Integrator(w.problem, w.dim, w.h, w.nsteps, w.batch, w.params, energy_every=10,
+                            balance=bal, schedule=sched, local_energy=True) as ig:
+            Y = torch.tensor(y, dtype=torch.float64, device="cuda")
+            ws = ig.new_workspace()
+            E = torch.zeros((ig.n_energy(), w.batch), dtype=torch.float64, device="cuda")
+            it = torch.zeros(w.batch, dtype=torch.int64, device="cuda")
+            ig.integrate(Y, ws, energy=E, iters=it)
+            rc, st = ig.stats(ws)
+            outs.append((Y.cpu().numpy(), E.cpu().numpy(), it.cpu().numpy(), st,
+                         ig.local_energy_error(ws).cpu().numpy(), rc))
+    for o in outs[1:]:
+        assert np.array_equal(o[0], outs[0][0], equal_nan=True)
+        assert np.array_equal(o[1], outs[0][1], equal_nan=True)
+        assert np.array_equal(o[2], outs[0][2]) and o[3] == outs[0][3]
+        assert np.array_equal(o[4], outs[0][4], equal_nan=True) and o[5] == outs[0][5]
+    assert outs[1][5] == irk.E_DIVERGED and outs[1][3]["diverged_traj"] == 2
+    idx = np.r_[5, 69990, np.arange(0, w.batch, 1009)]
+    orr = orc.integrate(w.problem, y[:, idx], w.params, w.h, w.nsteps, energy_every=10, local_energy=True)
+    assert np.array_equal(outs[1][0][:, idx], orr["y"], equal_nan=True)
+    assert np.array_equal(outs[1][1][:, idx], orr["energy"], equal_nan=True)
+    assert np.array_equal(outs[1][2][idx], orr["iters"])
+    assert np.array_equal(outs[1][4][idx], orr["dhloc"], equal_nan=True)
+
+
 # ------------------------------------------------------------------ config 3
 def test_config3_six_body_ragged_energy(irk, orc):
     """Config-3 generator, ragged batch of 37 members, 3,000 steps, energy every

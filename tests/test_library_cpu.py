@@ -61,6 +61,7 @@ def test_library_tableau_bitwise_equals_oracle_and_mpmath(irk, orc):
     (1, 4, float("nan"), 10, 4),
     (1, 4, 0.1, -1, 4),          # nsteps < 0
     (1, 4, 0.1, 10, 0),          # batch < 1
+    (1, 4, 0.1, 10, 2**31),      # batch > 2^31 - 1 (int32 trajectory indices)
     (9, 4, 0.1, 10, 4),          # unknown problem
     (2, 13, 0.1, 10, 4),         # N-body dim % 6
     (2, 42, 0.1, 10, 4),         # N-body ensembles: N = 7 unsupported
