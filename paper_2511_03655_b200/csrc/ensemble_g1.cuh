@@ -327,13 +327,26 @@ struct QueueArgs {
 };
 
 __device__ __forceinline__ int64_t dbits(double x) { return __double_as_longlong(x); }
-// |a - b| as bits, NaN -> 0 (the NaN-ignoring max never selects a NaN)
+// |a - b| as bits (NaN stays above +inf: a NaN-ignoring max is taken separately)
 __device__ __forceinline__ int64_t absdiff_bits(double a, double b) {
-    const int64_t e = dbits(dsub(a, b)) & 0x7fffffffffffffffLL;
-    return (e > 0x7ff0000000000000LL) ? 0 : e;
+    return dbits(dsub(a, b)) & 0x7fffffffffffffffLL;
 }
 __device__ __forceinline__ int64_t imax64(int64_t a, int64_t b) { return a > b ? a : b; }
 __device__ __forceinline__ int64_t imin64(int64_t a, int64_t b) { return a < b ? a : b; }
+constexpr int64_t kInfBits = 0x7ff0000000000000LL;
+// Delta = NaN-ignoring max of eight |differences| (the canonical left-to-right
+// `(e > d) ? e : d` from d = 0).  Plain max first; only if it is a NaN pattern
+// (a diverging trajectory) are the NaNs dropped, so the common case costs 7
+// int64 max operations.
+__device__ __forceinline__ int64_t delta_bits8(const int64_t *e) {
+    int64_t t = imax64(imax64(imax64(e[0], e[1]), imax64(e[2], e[3])), imax64(imax64(e[4], e[5]), imax64(e[6], e[7])));
+    if (t > kInfBits) {
+        t = 0;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) t = (e[i] > kInfBits) ? t : imax64(t, e[i]);
+    }
+    return t;
+}
 
 template <class P>
 __global__ void __maxnreg__(G1_MAXREG) ens_g1q_kernel(const __grid_constant__ EnsArgs a,
@@ -341,8 +354,13 @@ __global__ void __maxnreg__(G1_MAXREG) ens_g1q_kernel(const __grid_constant__ En
                                                      const __grid_constant__ P prob) {
     constexpr int d = P::d, D = 2 * d;
     const int64_t B = a.batch;
-    __shared__ __align__(16) double sW[2][64];  // [0] = mu~, [1] = nu~ (row-major)
-    for (int e = threadIdx.x; e < 128; e += blockDim.x) sW[e >> 6][e & 63] = (e < 64) ? (&c_mu[0][0])[e] : (&c_nu[0][0])[e - 64];
+    // mu~ at [0, 64), nu~ at [66, 130): the 2-double gap puts the two tables in
+    // different banks, so the per-lane (mu or nu) LDS.128 of a4 is conflict-free
+    // (unpadded: 7.65 instead of 3.9 shared wavefronts per load, ncu)
+    constexpr int kNuOff = 66;
+    __shared__ __align__(16) double sW[kNuOff + 64];
+    for (int e = threadIdx.x; e < 128; e += blockDim.x)
+        sW[(e < 64) ? e : kNuOff + e - 64] = (e < 64) ? (&c_mu[0][0])[e] : (&c_nu[0][0])[e - 64];
     __syncthreads();
     __shared__ double sQ[8 * d][G1_THREADS], sL[8 * d][G1_THREADS];
     __shared__ int64_t sM[d][G1_THREADS], sP[d][G1_THREADS];
@@ -350,21 +368,23 @@ __global__ void __maxnreg__(G1_MAXREG) ens_g1q_kernel(const __grid_constant__ En
     const int64_t n0 = *a.n_done;
     const bool sample = (a.energy != nullptr) && (a.energy_every > 0);
     const int64_t total = B * qa.nchunks;
-    const int64_t kInfBits = 0x7ff0000000000000LL;
 
     double q[d], v[d], V[8][d];
     int32_t b = -1;  // trajectory of the held unit (-1: none)
     int64_t c = 0, len = 0, n = 0, hits = 0, sweeps = 0, u = -1;
     double hprev = 0.0, dhmax = 0.0;
     int k = 0;
+    int32_t bb = 0;
     for (;;) {
         if (b < 0) {  // ---- acquire the next unit (divergent, once per unit) ----
-            if (u < 0) u = (int64_t)atomicAdd(qa.counter, 1ull);
-            if (u >= total) break;
-            c = u / B;
-            const int32_t bb = (int32_t)(u - c * B);
+            if (u < 0) {
+                u = (int64_t)atomicAdd(qa.counter, 1ull);
+                if (u >= total) break;
+                c = u / B;
+                bb = (int32_t)(u - c * B);
+            }
             if (c > 0 && ld_acquire(&qa.progress[bb]) < c) {  // predecessor unit still running
-                __nanosleep(256);
+                __nanosleep(1024);
                 continue;
             }
             u = -1;
@@ -447,9 +467,7 @@ __global__ void __maxnreg__(G1_MAXREG) ens_g1q_kernel(const __grid_constant__ En
                 }
             }
 #pragma unroll
-            for (int l = 0; l < d; ++l)
-                delta[l] = imax64(imax64(imax64(ev[l][0], ev[l][1]), imax64(ev[l][2], ev[l][3])),
-                                  imax64(imax64(ev[l][4], ev[l][5]), imax64(ev[l][6], ev[l][7])));
+            for (int l = 0; l < d; ++l) delta[l] = delta_bits8(ev[l]);
         }
         if (k >= 2) {  // a5, reading R2 (Delta^[k] exists from k = 2), on the bit patterns
 #pragma unroll
@@ -541,7 +559,7 @@ __global__ void __maxnreg__(G1_MAXREG) ens_g1q_kernel(const __grid_constant__ En
         }
         // a4 (second half) / next step's a1: V_i = v + D(W_i., Lv), W = fin ? nu : mu
         {
-            const double2 *W = reinterpret_cast<const double2 *>(&sW[fin ? 1 : 0][0]);
+            const double2 *W = reinterpret_cast<const double2 *>(&sW[fin ? kNuOff : 0]);
 #pragma unroll
             for (int i = 0; i < 8; ++i) {
                 double2 w[4];

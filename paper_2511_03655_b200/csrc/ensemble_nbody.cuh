@@ -13,11 +13,15 @@
 //
 // Canonical RHS (R-8, oracle accel_nbody_pairs): body k accumulates
 // its acceleration over the pairs that contain it in lexicographic pair order,
-// i.e. over j = 0..NB-1, j != k ascending, with d = q_k - q_j and
-// s = -(m_j w) for j < k, d = q_j - q_k and s = m_j w for j > k,
+// i.e. over j = 0..NB-1, j != k ascending; the oracle uses d = q_k - q_j,
+// s = -(m_j w) for j < k and d = q_j - q_k, s = m_j w for j > k, with
 // w = G / (r2 sqrt(r2)), r2 = fma(dz,dz,fma(dy,dy,fma(dx,dx,eps^2))),
-// a_k = fma(s, d, a_k).  Both lanes of a pair evaluate w with identical
-// operations, so the sum is bitwise the oracle's.
+// a_k = fma(s, d, a_k).  Here every partner uses d = q_j - q_k and s = m_j w:
+// RN(q_k - q_j) = -RN(q_j - q_k) and fma(-s, -d, a) = fma(s, d, a) exactly; the
+// one exception, q_j = q_k (both differences +0), only changes the sign of a
+// zero product, which cannot change a (a starts at +0 and is never -0).  r2
+// and w are symmetric, and both lanes of a pair evaluate w with identical
+// operations, so the sum is bitwise the oracle's without per-lane selects.
 //
 // The loop is warp-uniform (it runs until every group of the warp is done;
 // finished groups idle) so that __syncwarp / __ballot_sync always see the full
@@ -80,7 +84,12 @@ __global__ void __maxnreg__(NB_MAXREG) ens_nbody_kernel(const __grid_constant__ 
     const int64_t B = a.batch;
 
     __shared__ __align__(16) double sW[2][64];         // mu~, nu~ for the per-group choice in a4
-    __shared__ double sQ[GPB][8][d];                    // Q^[k] of every body and stage (+ Q^[k-1] for Delta)
+    // Q^[k] of every body and stage (+ Q^[k-1] for Delta).  Group stride GS = 8d
+    // padded to 5 (mod 16) doubles: the 5 groups of a warp read the same
+    // relative offsets, which an unpadded 8d = 0 (mod 16) stride would put in one
+    // 64-bit bank (5-way conflicts; ncu: 2.7x the ideal shared wavefronts).
+    constexpr int GS = 8 * d + (((5 - 8 * d) % 16) + 16) % 16;
+    __shared__ double sQ[GPB * GS];
     __shared__ double sQV[GPB][D];                      // (q, v) gathered for energy samples
     __shared__ double sm[NB];
     for (int e = threadIdx.x; e < 128; e += blockDim.x)
@@ -194,9 +203,9 @@ __global__ void __maxnreg__(NB_MAXREG) ens_nbody_kernel(const __grid_constant__ 
                     }
                     const double qn = dadd(q[c], acc);
                     if (lane_ok) {
-                        const double e = dabs(dsub(qn, sQ[gib][i][3 * body + c]));  // unused at k = 1
+                        const double e = dabs(dsub(qn, sQ[gib * GS + i * d + 3 * body + c]));  // unused at k = 1
                         delta[c] = (e > delta[c]) ? e : delta[c];
-                        sQ[gib][i][3 * body + c] = qn;
+                        sQ[gib * GS + i * d + 3 * body + c] = qn;
                     }
                 }
             }
@@ -222,21 +231,16 @@ __global__ void __maxnreg__(NB_MAXREG) ens_nbody_kernel(const __grid_constant__ 
         bool okdiv = true;
 #pragma unroll kNbRhsUnroll
         for (int i = 0; i < 8; ++i) {
-            const double *Qi = sQ[gib][i];
+            const double *Qi = &sQ[gib * GS + i * d];
             const double qx = Qi[3 * body], qy = Qi[3 * body + 1], qz = Qi[3 * body + 2];
             double ax = 0.0, ay = 0.0, az = 0.0;
 #pragma unroll
             for (int o = 0; o < NB - 1; ++o) {
-                const bool lo = o < body;          // partner j = o (j < k) or o + 1 (j > k)
-                const int j = lo ? o : o + 1;
-                const double jx = Qi[3 * j], jy = Qi[3 * j + 1], jz = Qi[3 * j + 2];
-                const double dx = lo ? dsub(qx, jx) : dsub(jx, qx);
-                const double dy = lo ? dsub(qy, jy) : dsub(jy, qy);
-                const double dz = lo ? dsub(qz, jz) : dsub(jz, qz);
+                const int j = (o < body) ? o : o + 1;  // partners in ascending order
+                const double dx = dsub(Qi[3 * j], qx), dy = dsub(Qi[3 * j + 1], qy), dz = dsub(Qi[3 * j + 2], qz);
                 const double r2 = dfma(dz, dz, dfma(dy, dy, dfma(dx, dx, P.eps2)));
                 const double w = ddiv_fast(P.G, dmul(r2, dsqrt_fast(r2, okdiv)), okdiv);
-                const double mw = dmul(sm[j], w);
-                const double s = lo ? -mw : mw;
+                const double s = dmul(sm[j], w);
                 ax = dfma(s, dx, ax);
                 ay = dfma(s, dy, ay);
                 az = dfma(s, dz, az);
@@ -245,24 +249,20 @@ __global__ void __maxnreg__(NB_MAXREG) ens_nbody_kernel(const __grid_constant__ 
             Lv[i][1] = dmul(a.hb[i], ay);
             Lv[i][2] = dmul(a.hb[i], az);
         }
-        if (__any_sync(FULL, live && !okdiv)) {  // exact-intrinsic re-evaluation (same bits)
-#pragma unroll 1
+        if (__any_sync(FULL, live && !okdiv)) {  // exact-intrinsic re-evaluation (same bits);
+                                                 // unrolled so that Lv stays in registers
+#pragma unroll
             for (int i = 0; i < 8; ++i) {
-                const double *Qi = sQ[gib][i];
+                const double *Qi = &sQ[gib * GS + i * d];
                 const double qx = Qi[3 * body], qy = Qi[3 * body + 1], qz = Qi[3 * body + 2];
                 double ax = 0.0, ay = 0.0, az = 0.0;
 #pragma unroll
                 for (int o = 0; o < NB - 1; ++o) {
-                    const bool lo = o < body;
-                    const int j = lo ? o : o + 1;
-                    const double jx = Qi[3 * j], jy = Qi[3 * j + 1], jz = Qi[3 * j + 2];
-                    const double dx = lo ? dsub(qx, jx) : dsub(jx, qx);
-                    const double dy = lo ? dsub(qy, jy) : dsub(jy, qy);
-                    const double dz = lo ? dsub(qz, jz) : dsub(jz, qz);
+                    const int j = (o < body) ? o : o + 1;
+                    const double dx = dsub(Qi[3 * j], qx), dy = dsub(Qi[3 * j + 1], qy), dz = dsub(Qi[3 * j + 2], qz);
                     const double r2 = dfma(dz, dz, dfma(dy, dy, dfma(dx, dx, P.eps2)));
                     const double w = ddiv(P.G, dmul(r2, dsqrt(r2)));
-                    const double mw = dmul(sm[j], w);
-                    const double s = lo ? -mw : mw;
+                    const double s = dmul(sm[j], w);
                     ax = dfma(s, dx, ax);
                     ay = dfma(s, dy, ay);
                     az = dfma(s, dz, az);
