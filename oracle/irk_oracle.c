@@ -280,28 +280,32 @@ static void accel_fpu(int N, const double *P, const double *q, double *a) {
     }
 }
 
-/* N-body, symmetric pairs i<j in lexicographic order (Eq. Ham2):
+/* N-body ensembles (Eq. Ham2), cyclic partner order (CANON.md):
  *   d = q_j - q_i; r2 = fma(dz,dz,fma(dy,dy,fma(dx,dx,eps^2))); w = G/(r2*sqrt(r2));
- *   a_i = fma(m_j*w, d, a_i); a_j = fma(-(m_i*w), d, a_j). */
+ *   a_i = fma(m_j*w, d, a_i) for j = (i+1)%N, (i+2)%N, ..., (i+N-1)%N. */
 static void accel_nbody_pairs(int N, const double *P, const double *q, double *a) {
+    /* Eq. Ham2 force on each body i: the sum over the other bodies j
+     * taken in cyclic order j = (i + delta) mod N, delta = 1..N-1 (R-8;
+     * the paper does not fix a summation order). */
     double G = P[0], eps2 = P[1] * P[1];
     const double *m = P + 2;
-    for (int k = 0; k < 3 * N; ++k) a[k] = 0.0;
     for (int i = 0; i < N; ++i) {
-        for (int j = i + 1; j < N; ++j) {
+        double ax = 0.0, ay = 0.0, az = 0.0;
+        for (int delta = 1; delta < N; ++delta) {
+            int j = (i + delta) % N;
             double dx = q[3 * j] - q[3 * i];
             double dy = q[3 * j + 1] - q[3 * i + 1];
             double dz = q[3 * j + 2] - q[3 * i + 2];
             double r2 = fma(dz, dz, fma(dy, dy, fma(dx, dx, eps2)));
             double w = G / (r2 * sqrt(r2));
-            double si = m[j] * w, sj = -(m[i] * w);
-            a[3 * i] = fma(si, dx, a[3 * i]);
-            a[3 * i + 1] = fma(si, dy, a[3 * i + 1]);
-            a[3 * i + 2] = fma(si, dz, a[3 * i + 2]);
-            a[3 * j] = fma(sj, dx, a[3 * j]);
-            a[3 * j + 1] = fma(sj, dy, a[3 * j + 1]);
-            a[3 * j + 2] = fma(sj, dz, a[3 * j + 2]);
+            double s = m[j] * w;
+            ax = fma(s, dx, ax);
+            ay = fma(s, dy, ay);
+            az = fma(s, dz, az);
         }
+        a[3 * i] = ax;
+        a[3 * i + 1] = ay;
+        a[3 * i + 2] = az;
     }
 }
 

@@ -21,7 +21,7 @@ extern "C" {
 /* Problem ids (same numbering as include/irk.h; the numbers are the only
  * thing the two sides agree on, by documentation, not by a shared header). */
 #define ORC_KEPLER 1        /* planar Kepler, d=2, params {GM}                      */
-#define ORC_NBODY 2         /* N-body, symmetric pairs, params {G, eps, m_1..m_N}  */
+#define ORC_NBODY 2         /* N-body, cyclic pair order, params {G, eps, m_1..m_N} */
 #define ORC_FPU_BETA 3      /* FPU-beta chain, fixed ends, params {beta}           */
 #define ORC_HENON_HEILES 4  /* Listing 2, params {lambda, xi}         */
 #define ORC_NBODY_DIRECT 5  /* large-N direct sum, blocked j-order, {G, eps>0, m}  */

@@ -11,17 +11,15 @@
 // group exchanges through a shared-memory tile that doubles as Q^[k-1] for the
 // stop test.
 //
-// Canonical RHS (R-8, oracle accel_nbody_pairs): body k accumulates
-// its acceleration over the pairs that contain it in lexicographic pair order,
-// i.e. over j = 0..NB-1, j != k ascending; the oracle uses d = q_k - q_j,
-// s = -(m_j w) for j < k and d = q_j - q_k, s = m_j w for j > k, with
-// w = G / (r2 sqrt(r2)), r2 = fma(dz,dz,fma(dy,dy,fma(dx,dx,eps^2))),
-// a_k = fma(s, d, a_k).  Here every partner uses d = q_j - q_k and s = m_j w:
-// RN(q_k - q_j) = -RN(q_j - q_k) and fma(-s, -d, a) = fma(s, d, a) exactly; the
-// one exception, q_j = q_k (both differences +0), only changes the sign of a
-// zero product, which cannot change a (a starts at +0 and is never -0).  r2
-// and w are symmetric, and both lanes of a pair evaluate w with identical
-// operations, so the sum is bitwise the oracle's without per-lane selects.
+// Canonical RHS (R-8, oracle accel_nbody_pairs): body k sums over its
+// partners j = (k + delta) mod NB in the cyclic order delta = 1..NB-1, with
+// d = q_j - q_k, r2 = fma(dz,dz,fma(dy,dy,fma(dx,dx,eps^2))),
+// w = G / (r2 sqrt(r2)), a_k = fma(m_j w, d, a_k).  The pair weight w is
+// symmetric in (k, j) bit for bit (the two differences are exact negatives), so
+// each lane evaluates it only for delta = 1..NB/2 and takes delta > NB/2 -- the
+// pair (k - o, k), o = NB - delta -- from lane k - o by a warp shuffle: 3 weight
+// evaluations per lane and stage for NB = 6 instead of 5, every lane running the
+// same delta sequence (no per-lane selects).
 //
 // The loop is warp-uniform (it runs until every group of the warp is done;
 // finished groups idle) so that __syncwarp / __ballot_sync always see the full
@@ -66,11 +64,52 @@ __device__ double nbody_energy(const double *qv, const NBodyParams &P) {
     return tot.result();
 }
 
+// Acceleration of body `body` at one stage (canonical RHS, see the header).
+template <int NB, bool EXACT>
+__device__ __forceinline__ void nb_stage_accel(const double *Qi, int body, int lane, const NBodyParams &P,
+                                               const double *sm, bool &ok, double &ax, double &ay, double &az) {
+    const double qx = Qi[3 * body], qy = Qi[3 * body + 1], qz = Qi[3 * body + 2];
+    ax = 0.0, ay = 0.0, az = 0.0;
+    // partners j = (k + delta) mod NB, delta = 1..NB-1.  Offsets delta <= NB/2 are
+    // evaluated here; delta > NB/2 is the pair (k - o, k), o = NB - delta, whose
+    // weight lane k - o evaluated as its offset o: fetched by shuffle.
+    constexpr int HF = NB / 2, HB = (NB - 1) / 2;
+    double wf[HF + 1], dfx[HF + 1], dfy[HF + 1], dfz[HF + 1];
+#pragma unroll
+    for (int o = 1; o <= HF; ++o) {
+        const int j = (body + o < NB) ? body + o : body + o - NB;
+        dfx[o] = dsub(Qi[3 * j], qx), dfy[o] = dsub(Qi[3 * j + 1], qy), dfz[o] = dsub(Qi[3 * j + 2], qz);
+        const double r2 = dfma(dfz[o], dfz[o], dfma(dfy[o], dfy[o], dfma(dfx[o], dfx[o], P.eps2)));
+        wf[o] = EXACT ? ddiv(P.G, dmul(r2, dsqrt(r2))) : ddiv_fast(P.G, dmul(r2, dsqrt_fast(r2, ok)), ok);
+    }
+    double wb[HB + 1];
+#pragma unroll
+    for (int o = 1; o <= HB; ++o) {
+        const int src = lane - body + ((body - o >= 0) ? body - o : body - o + NB);
+        wb[o] = __shfl_sync(0xffffffffu, wf[o], src & 31);
+    }
+#pragma unroll
+    for (int delta = 1; delta < NB; ++delta) {
+        const int j = (body + delta < NB) ? body + delta : body + delta - NB;
+        double dx, dy, dz, w;
+        if (delta <= HF) {
+            dx = dfx[delta], dy = dfy[delta], dz = dfz[delta], w = wf[delta];
+        } else {
+            dx = dsub(Qi[3 * j], qx), dy = dsub(Qi[3 * j + 1], qy), dz = dsub(Qi[3 * j + 2], qz);
+            w = wb[NB - delta];
+        }
+        const double s = dmul(sm[j], w);
+        ax = dfma(s, dx, ax);
+        ay = dfma(s, dy, ay);
+        az = dfma(s, dz, az);
+    }
+}
+
 #ifndef NB_MAXREG
 #define NB_MAXREG 168  // config 3, 5,000 steps: 168 -> 306 ms, 255 -> 309, 128 -> 342 (tools/variants.py)
 #endif
 #ifndef NB_RHS_UNROLL
-#define NB_RHS_UNROLL 2  // stages of the RHS loop in flight
+#define NB_RHS_UNROLL 4  // stages of the RHS loop in flight (config 3, 5,000 steps: 2 -> 235 ms, 4 -> 230)
 #endif
 constexpr int kNbRhsUnroll = NB_RHS_UNROLL;
 
@@ -225,48 +264,23 @@ __global__ void __maxnreg__(NB_MAXREG) ens_nbody_kernel(const __grid_constant__ 
         const unsigned notok = __ballot_sync(FULL, !ok_lane);
         const bool stop = (k >= 2) && ((notok & gmask) == 0u);
         __syncwarp();  // every body's Q^[k] is in sQ
-        // ---- a3: F_i(body) = sum over the pairs containing it, lexicographic order ----
+        // ---- a3: F_i(body) = sum over the other bodies, cyclic order (header) ----
         const double tn1 = dadd(a.t0, dmul((double)(n0 + n), a.h));
         (void)tn1;  // the N-body RHS is autonomous
         bool okdiv = true;
 #pragma unroll kNbRhsUnroll
         for (int i = 0; i < 8; ++i) {
-            const double *Qi = &sQ[gib * GS + i * d];
-            const double qx = Qi[3 * body], qy = Qi[3 * body + 1], qz = Qi[3 * body + 2];
-            double ax = 0.0, ay = 0.0, az = 0.0;
-#pragma unroll
-            for (int o = 0; o < NB - 1; ++o) {
-                const int j = (o < body) ? o : o + 1;  // partners in ascending order
-                const double dx = dsub(Qi[3 * j], qx), dy = dsub(Qi[3 * j + 1], qy), dz = dsub(Qi[3 * j + 2], qz);
-                const double r2 = dfma(dz, dz, dfma(dy, dy, dfma(dx, dx, P.eps2)));
-                const double w = ddiv_fast(P.G, dmul(r2, dsqrt_fast(r2, okdiv)), okdiv);
-                const double s = dmul(sm[j], w);
-                ax = dfma(s, dx, ax);
-                ay = dfma(s, dy, ay);
-                az = dfma(s, dz, az);
-            }
+            double ax, ay, az;
+            nb_stage_accel<NB, false>(&sQ[gib * GS + i * d], body, lane, P, sm, okdiv, ax, ay, az);
             Lv[i][0] = dmul(a.hb[i], ax);
             Lv[i][1] = dmul(a.hb[i], ay);
             Lv[i][2] = dmul(a.hb[i], az);
         }
-        if (__any_sync(FULL, live && !okdiv)) {  // exact-intrinsic re-evaluation (same bits);
-                                                 // unrolled so that Lv stays in registers
+        if (__any_sync(FULL, live && !okdiv)) {  // exact-intrinsic re-evaluation (same bits)
 #pragma unroll
             for (int i = 0; i < 8; ++i) {
-                const double *Qi = &sQ[gib * GS + i * d];
-                const double qx = Qi[3 * body], qy = Qi[3 * body + 1], qz = Qi[3 * body + 2];
-                double ax = 0.0, ay = 0.0, az = 0.0;
-#pragma unroll
-                for (int o = 0; o < NB - 1; ++o) {
-                    const int j = (o < body) ? o : o + 1;
-                    const double dx = dsub(Qi[3 * j], qx), dy = dsub(Qi[3 * j + 1], qy), dz = dsub(Qi[3 * j + 2], qz);
-                    const double r2 = dfma(dz, dz, dfma(dy, dy, dfma(dx, dx, P.eps2)));
-                    const double w = ddiv(P.G, dmul(r2, dsqrt(r2)));
-                    const double s = dmul(sm[j], w);
-                    ax = dfma(s, dx, ax);
-                    ay = dfma(s, dy, ay);
-                    az = dfma(s, dz, az);
-                }
+                double ax, ay, az;
+                nb_stage_accel<NB, true>(&sQ[gib * GS + i * d], body, lane, P, sm, okdiv, ax, ay, az);
                 Lv[i][0] = dmul(a.hb[i], ax);
                 Lv[i][1] = dmul(a.hb[i], ay);
                 Lv[i][2] = dmul(a.hb[i], az);

@@ -308,7 +308,7 @@ def test_rhs_is_minus_grad_U(orc, problem, dim, params):
 
 
 def test_direct_and_pair_nbody_agree(orc):
-    """The two canonical N-body sequences (symmetric pairs, blocked direct sum)
+    """The two canonical N-body sequences (cyclic pairs, blocked direct sum)
     evaluate the same formula Eq. Ham2: agree to a few ulp of the force scale."""
     g = np.random.default_rng(9)
     N = 40
