@@ -39,6 +39,15 @@ __device__ __forceinline__ void dhloc_update(double hn, double &hprev, double &d
     dmax = (loc > dmax) ? loc : dmax;
     hprev = hn;
 }
+// Work queue of the persistent ensemble kernels (ens_g1q, ens_chain_q): units
+// u = c * batch + b are (trajectory b, step chunk c of qchunk steps).
+struct QueueArgs {
+    unsigned long long *counter;  // next unit
+    int32_t *progress;            // [batch] chunks completed in this call
+    int64_t qchunk;               // steps per unit
+    int64_t nchunks;              // units per trajectory
+};
+
 // inter-unit hand-off of the work-queue kernels (gpu-scope release / acquire)
 __device__ __forceinline__ int32_t ld_acquire(const int32_t *p) {
     int32_t v;

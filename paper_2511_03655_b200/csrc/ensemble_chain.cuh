@@ -41,31 +41,31 @@ __device__ double fpu_energy(const double *q, const double *v, double beta) {
     return n.result();
 }
 
+// Site index -> shared-memory slot of a chain's stage tile: site L*SPL + s of lane L
+// lives at s*32 + L, so own-site and neighbour-site accesses of a warp hit 32
+// consecutive doubles (conflict-free; the site-major layout was 2-way conflicted
+// for SPL = 2).
 template <int SPL>
-__global__ void __launch_bounds__(CH_THREADS) ens_chain_kernel(const __grid_constant__ EnsArgs a, const double beta) {
-    constexpr int N = 32 * SPL, d = N, D = 2 * N, CPB = CH_THREADS / 32;
+__device__ __forceinline__ int ch_slot(int site) { return (site % SPL) * 32 + site / SPL; }
+
+// One warp integrates chain b over the call-local steps [c0, c0 + nsteps).
+template <int SPL>
+__device__ __forceinline__ void chain_unit(const EnsArgs &a, const double beta, const int64_t b, const int64_t c0,
+                                           const int64_t nsteps, double (*sQ)[32 * SPL], double *sQV,
+                                           const double (*sW)[64]) {
+    constexpr int N = 32 * SPL, d = N, D = 2 * N;
     const unsigned FULL = 0xffffffffu;
     const int64_t B = a.batch;
-    __shared__ __align__(16) double sW[2][64];
-    __shared__ double sQ[CPB][8][N];   // Q^[k] of the chain (neighbour reads + Delta)
-    __shared__ double sQV[CPB][2 * N]; // (q, v) for energy samples
-    for (int e = threadIdx.x; e < 128; e += blockDim.x)
-        sW[e >> 6][e & 63] = (e < 64) ? (&c_mu[0][0])[e] : (&c_nu[0][0])[e - 64];
-    __syncthreads();
-    const int lane = threadIdx.x & 31, cib = threadIdx.x >> 5;
-    const int64_t slot = (int64_t)blockIdx.x * CPB + cib;
-    if (slot >= a.nslots) return;  // warp-uniform
-    const int64_t b = a.perm ? (int64_t)a.perm[slot] : slot;
-    if (b < 0 || b >= B) return;   // warp-uniform
+    const int lane = threadIdx.x & 31;
     const int s0 = lane * SPL;
 
     double q[SPL], v[SPL];
 #pragma unroll
-    for (int s = 0; s < SPL; ++s) {
-        q[s] = a.y[(int64_t)(s0 + s) * B + b];
-        v[s] = a.y[(int64_t)(d + s0 + s) * B + b];
+    for (int s = 0; s < SPL; ++s) {  // L2 loads: the previous unit may have run on another SM
+        q[s] = __ldcg(&a.y[(int64_t)(s0 + s) * B + b]);
+        v[s] = __ldcg(&a.y[(int64_t)(d + s0 + s) * B + b]);
     }
-    int64_t bad = a.stats[1 * B + b];
+    int64_t bad = __ldcg(&a.stats[1 * B + b]);
     const int64_t n0 = *a.n_done;
     const bool sample = (a.energy != nullptr) && (a.energy_every > 0);
     double hprev = 0.0, dhmax = 0.0;  // lane 0: DH^loc tracking
@@ -73,24 +73,24 @@ __global__ void __launch_bounds__(CH_THREADS) ens_chain_kernel(const __grid_cons
     auto energy_at = [&](int64_t idx, bool track) {
 #pragma unroll
         for (int s = 0; s < SPL; ++s) {
-            sQV[cib][s0 + s] = q[s];
-            sQV[cib][N + s0 + s] = v[s];
+            sQV[s0 + s] = q[s];
+            sQV[N + s0 + s] = v[s];
         }
         __syncwarp();
         if (lane == 0) {
-            const double hn = fpu_energy<N>(sQV[cib], sQV[cib] + N, beta);
+            const double hn = fpu_energy<N>(sQV, sQV + N, beta);
             if (idx >= 0) a.energy[idx * B + b] = hn;
             if (track) dhloc_update(hn, hprev, dhmax);
             else hprev = hn;
         }
         __syncwarp();
     };
-    if ((sample && a.c0 == 0) || a.local_energy) energy_at((sample && a.c0 == 0) ? 0 : -1, false);
-    if (bad > 0 || a.nsteps == 0) {
+    if ((sample && c0 == 0) || a.local_energy) energy_at((sample && c0 == 0) ? 0 : -1, false);
+    if (bad > 0 || nsteps == 0) {
         if (lane == 0) {
-            if (a.iters && a.c0 == 0) a.iters[b] = 0;
+            if (a.iters && c0 == 0) a.iters[b] = 0;
             if (a.csweeps) a.csweeps[b] = 0;
-            if (a.local_energy && a.c0 == 0) a.stats[3 * B + b] = 0;
+            if (a.local_energy && c0 == 0) a.stats[3 * B + b] = 0;
         }
         return;
     }
@@ -100,7 +100,7 @@ __global__ void __launch_bounds__(CH_THREADS) ens_chain_kernel(const __grid_cons
 #pragma unroll
         for (int j = 0; j < 8; ++j)
 #pragma unroll
-            for (int s = 0; s < SPL; ++s) H[j][s] = a.hist[((int64_t)j * D + d + s0 + s) * B + b];
+            for (int s = 0; s < SPL; ++s) H[j][s] = __ldcg(&a.hist[((int64_t)j * D + d + s0 + s) * B + b]);
 #pragma unroll
         for (int i = 0; i < 8; ++i)
 #pragma unroll
@@ -117,7 +117,7 @@ __global__ void __launch_bounds__(CH_THREADS) ens_chain_kernel(const __grid_cons
     for (int s = 0; s < SPL; ++s) m[s] = p[s] = kInf;
     int64_t n = 0, hits = 0, sweeps = 0;
     int k = 0;
-    while (n < a.nsteps) {  // warp-uniform
+    while (n < nsteps) {  // warp-uniform
         ++k;
         // a2 + Delta
         double Lq[8][SPL], sLq[SPL], delta[SPL];
@@ -150,9 +150,9 @@ __global__ void __launch_bounds__(CH_THREADS) ens_chain_kernel(const __grid_cons
                         acc = dfma(w[jj].y, Lq[2 * jj + 1][s], acc);
                     }
                     const double qn = dadd(q[s], acc);
-                    const double e = dabs(dsub(qn, sQ[cib][i][s0 + s]));
+                    const double e = dabs(dsub(qn, sQ[i][s * 32 + lane]));
                     delta[s] = (e > delta[s]) ? e : delta[s];
-                    sQ[cib][i][s0 + s] = qn;
+                    sQ[i][s * 32 + lane] = qn;
                 }
             }
         }
@@ -173,12 +173,12 @@ __global__ void __launch_bounds__(CH_THREADS) ens_chain_kernel(const __grid_cons
         double Lv[8][SPL];
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
-            const double *Qi = sQ[cib][i];
+            const double *Qi = sQ[i];
             double qs[SPL + 2];
-            qs[0] = (s0 == 0) ? 0.0 : Qi[s0 - 1];
+            qs[0] = (s0 == 0) ? 0.0 : Qi[ch_slot<SPL>(s0 - 1)];
 #pragma unroll
-            for (int s = 0; s < SPL; ++s) qs[s + 1] = Qi[s0 + s];
-            qs[SPL + 1] = (s0 + SPL == N) ? 0.0 : Qi[s0 + SPL];
+            for (int s = 0; s < SPL; ++s) qs[s + 1] = Qi[s * 32 + lane];
+            qs[SPL + 1] = (s0 + SPL == N) ? 0.0 : Qi[ch_slot<SPL>(s0 + SPL)];
             double f[SPL + 1];
 #pragma unroll
             for (int t = 0; t <= SPL; ++t) f[t] = fpu_bond(dsub(qs[t + 1], qs[t]), beta);
@@ -204,9 +204,9 @@ __global__ void __launch_bounds__(CH_THREADS) ens_chain_kernel(const __grid_cons
             k = 0;
 #pragma unroll
             for (int s = 0; s < SPL; ++s) m[s] = p[s] = kInf;
-            const bool due = sample && ((a.c0 + n) % a.energy_every) == 0;
-            if (due || a.local_energy) energy_at(due ? (a.c0 + n) / a.energy_every : -1, a.local_energy != 0);
-            if (n == a.nsteps || !finite) {
+            const bool due = sample && ((c0 + n) % a.energy_every) == 0;
+            if (due || a.local_energy) energy_at(due ? (c0 + n) / a.energy_every : -1, a.local_energy != 0);
+            if (n == nsteps || !finite) {
 #pragma unroll
                 for (int j = 0; j < 8; ++j)
 #pragma unroll
@@ -219,7 +219,7 @@ __global__ void __launch_bounds__(CH_THREADS) ens_chain_kernel(const __grid_cons
             }
         }
         {
-            const double2 *W = reinterpret_cast<const double2 *>(&sW[fin ? 1 : 0][0]);
+            const double2 *W = reinterpret_cast<const double2 *>(&sW[fin ? 1 : 0][0]);  // warp-uniform
 #pragma unroll
             for (int i = 0; i < 8; ++i) {
                 double2 w[4];
@@ -245,12 +245,69 @@ __global__ void __launch_bounds__(CH_THREADS) ens_chain_kernel(const __grid_cons
         a.y[(int64_t)(d + s0 + s) * B + b] = v[s];
     }
     if (lane == 0) {
-        a.stats[0 * B + b] += hits;
+        a.stats[0 * B + b] = __ldcg(&a.stats[0 * B + b]) + hits;
         a.stats[1 * B + b] = bad;
-        a.stats[2 * B + b] += sweeps;
-        if (a.iters) a.iters[b] = (a.c0 == 0) ? sweeps : a.iters[b] + sweeps;
+        a.stats[2 * B + b] = __ldcg(&a.stats[2 * B + b]) + sweeps;
+        if (a.iters) a.iters[b] = (c0 == 0) ? sweeps : __ldcg(&a.iters[b]) + sweeps;
         if (a.csweeps) a.csweeps[b] = (int32_t)sweeps;
-        if (a.local_energy) dhloc_store(&a.stats[3 * B + b], a.c0 == 0, dhmax);
+        if (a.local_energy) dhloc_store(&a.stats[3 * B + b], c0 == 0, dhmax);
+    }
+}
+
+#ifndef CH_MAXREG
+#define CH_MAXREG 255
+#endif
+template <int SPL>
+__global__ void __maxnreg__(CH_MAXREG) ens_chain_kernel(const __grid_constant__ EnsArgs a, const double beta) {
+    constexpr int N = 32 * SPL, CPB = CH_THREADS / 32;
+    __shared__ __align__(16) double sW[2][64];
+    __shared__ double sQ[CPB][8][N];   // Q^[k] of the chain (neighbour reads + Delta), slots ch_slot()
+    __shared__ double sQV[CPB][2 * N]; // (q, v) for energy samples
+    for (int e = threadIdx.x; e < 128; e += blockDim.x)
+        sW[e >> 6][e & 63] = (e < 64) ? (&c_mu[0][0])[e] : (&c_nu[0][0])[e - 64];
+    __syncthreads();
+    const int cib = threadIdx.x >> 5;
+    const int64_t slot = (int64_t)blockIdx.x * CPB + cib;
+    if (slot >= a.nslots) return;  // warp-uniform
+    const int64_t b = a.perm ? (int64_t)a.perm[slot] : slot;
+    if (b < 0 || b >= a.batch) return;   // warp-uniform
+    chain_unit<SPL>(a, beta, b, a.c0, a.nsteps, sQ[cib], sQV[cib], sW);
+}
+
+// Persistent work-queue version (IRK_OPT_SCHEDULE 0/2; see ens_g1q): every warp
+// pulls (chain, step-chunk) units until the queue drains; unit (b, c) waits for
+// progress[b] = c.  Same arithmetic per unit, so bitwise any schedule.
+#ifndef CHQ_MAXREG
+#define CHQ_MAXREG 176  // config 4 at 20,000 steps: 164 regs (unbounded) 371 ms, 174-176 regs 326 ms
+#endif
+template <int SPL>
+__global__ void __maxnreg__(CHQ_MAXREG) ens_chain_q_kernel(const __grid_constant__ EnsArgs a,
+                                                                const __grid_constant__ QueueArgs qa,
+                                                                const double beta) {
+    constexpr int N = 32 * SPL, CPB = CH_THREADS / 32;
+    __shared__ __align__(16) double sW[2][64];
+    __shared__ double sQ[CPB][8][N];
+    __shared__ double sQV[CPB][2 * N];
+    for (int e = threadIdx.x; e < 128; e += blockDim.x)
+        sW[e >> 6][e & 63] = (e < 64) ? (&c_mu[0][0])[e] : (&c_nu[0][0])[e - 64];
+    __syncthreads();
+    const int cib = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t B = a.batch, total = B * qa.nchunks;
+    for (;;) {
+        unsigned long long u = 0;
+        if (lane == 0) u = atomicAdd(qa.counter, 1ull);
+        u = __shfl_sync(0xffffffffu, u, 0);
+        if ((int64_t)u >= total) break;
+        const int64_t c = (int64_t)u / B, b = (int64_t)u - c * B;
+        if (lane == 0 && c > 0)
+            while (ld_acquire(&qa.progress[b]) < c) __nanosleep(1024);
+        __syncwarp();
+        const int64_t c0 = c * qa.qchunk;
+        const int64_t len = (a.nsteps - c0 < qa.qchunk) ? a.nsteps - c0 : qa.qchunk;
+        chain_unit<SPL>(a, beta, b, c0, len, sQ[cib], sQV[cib], sW);
+        __threadfence();  // this warp's stores of the unit, before the hand-off
+        __syncwarp();
+        if (lane == 0) st_release(&qa.progress[b], (int32_t)(c + 1));
     }
 }
 

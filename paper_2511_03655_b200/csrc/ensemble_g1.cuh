@@ -319,12 +319,6 @@ namespace irk {
 // non-negative, non-NaN double (|.|, NaN mapped to 0 as the canonical
 // NaN-ignoring max does, +inf for "no history"), whose IEEE order is the order
 // of the bit patterns as int64.
-struct QueueArgs {
-    unsigned long long *counter;  // next unit
-    int32_t *progress;            // [batch] chunks completed in this call
-    int64_t qchunk;               // steps per unit
-    int64_t nchunks;              // units per trajectory
-};
 
 __device__ __forceinline__ int64_t dbits(double x) { return __double_as_longlong(x); }
 // |a - b| as bits (NaN stays above +inf: a NaN-ignoring max is taken separately)

@@ -32,7 +32,8 @@ struct irk_ctx {
     int mode = 0, max_iters = 100, mapping = 0;
     int64_t balance = -1;  // IRK_OPT_BALANCE: -1 auto, 0 off, >0 chunk length
     int schedule = 0;      // IRK_OPT_SCHEDULE: 0 auto, 1 chunked launches, 2 persistent work queue
-    int g1q_blocks_per_sm = 0;  // occupancy of ens_g1q (queried once)
+    int g1q_blocks_per_sm = 0;  // occupancy of the work-queue kernels (queried once)
+    int chain_blocks_per_sm[5] = {0, 0, 0, 0, 0};
     int local_energy = 0;  // IRK_OPT_LOCAL_ENERGY
     int64_t energy_every = 0;
     Tableau T;
@@ -334,30 +335,29 @@ EnsArgs ens_args(irk_ctx *c, double *y, double t0, char *ws, double *energy, int
     return a;
 }
 
-// Persistent work-queue launch of the g1 mapping (ensemble_g1.cuh, ens_g1q):
-// grid = resident capacity, units of `qchunk` steps per trajectory.
-template <class P>
-int launch_g1q(irk_ctx *c, const P &prob, EnsArgs &a, char *ws, cudaStream_t st) {
+// Persistent work-queue launches (IRK_OPT_SCHEDULE auto / 2): grid = resident
+// capacity of `kernel`, `spb` trajectory slots per block; units of `qchunk` steps
+// (one unit per trajectory when every trajectory has its own slot, else ~32).
+template <class KernelPtr, class LaunchFn>
+int launch_queue(irk_ctx *c, KernelPtr kernel, int threads, int spb, int *bps_cache, EnsArgs &a, char *ws,
+                 cudaStream_t st, LaunchFn launch) {
     int rc;
-    if (!c->g1q_blocks_per_sm &&
-        (rc = cuda_check(c, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c->g1q_blocks_per_sm, irk::ens_g1q_kernel<P>,
-                                                                           irk::G1_THREADS, 0),
-                         "occupancy")))
+    if (!*bps_cache &&
+        (rc = cuda_check(c, cudaOccupancyMaxActiveBlocksPerMultiprocessor(bps_cache, kernel, threads, 0), "occupancy")))
         return rc;
     int dev = 0, sms = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    const int64_t lanes = (int64_t)sms * (c->g1q_blocks_per_sm > 0 ? c->g1q_blocks_per_sm : 1) * irk::G1_THREADS;
-    const int64_t need = (c->batch + irk::G1_THREADS - 1) / irk::G1_THREADS;
-    const int64_t blocks = need < lanes / irk::G1_THREADS ? need : lanes / irk::G1_THREADS;
+    const int64_t resident_blocks = (int64_t)sms * (*bps_cache > 0 ? *bps_cache : 1);
+    const int64_t need = (c->batch + spb - 1) / spb;
+    const int64_t blocks = need < resident_blocks ? need : resident_blocks;
     irk::QueueArgs qa;
     Sched sc = sched_of(c, ws);
     qa.progress = sc.perm;
     qa.counter = reinterpret_cast<unsigned long long *>(sc.bins);
-    // one unit per trajectory when every trajectory has its own lane; else ~32 units each
     int64_t chunk = c->nsteps;
     if (c->balance > 0) chunk = c->balance;
-    else if (c->balance < 0 && c->batch > lanes) chunk = (c->nsteps + 31) / 32;
+    else if (c->balance < 0 && c->batch > resident_blocks * spb) chunk = (c->nsteps + 31) / 32;
     if (chunk < 1) chunk = 1;
     qa.qchunk = chunk;
     qa.nchunks = c->nsteps > 0 ? (c->nsteps + chunk - 1) / chunk : 1;
@@ -368,10 +368,18 @@ int launch_g1q(irk_ctx *c, const P &prob, EnsArgs &a, char *ws, cudaStream_t st)
     a.nslots = c->batch;
     if ((rc = cuda_check(c, cudaMemsetAsync(sc.perm, 0, sizeof(int32_t) * c->batch, st), "memset progress"))) return rc;
     if ((rc = cuda_check(c, cudaMemsetAsync(sc.bins, 0, sizeof(unsigned long long), st), "memset counter"))) return rc;
-    irk::ens_g1q_kernel<P><<<(unsigned)blocks, irk::G1_THREADS, 0, st>>>(a, qa, prob);
-    if ((rc = cuda_check(c, cudaGetLastError(), "ens_g1q launch"))) return rc;
+    launch(a, qa, (unsigned)blocks);
+    if ((rc = cuda_check(c, cudaGetLastError(), "work-queue kernel launch"))) return rc;
     advance_n_kernel<<<1, 1, 0, st>>>(reinterpret_cast<int64_t *>(ws), c->nsteps);
     return cuda_check(c, cudaGetLastError(), "advance_n launch");
+}
+
+template <class P>
+int launch_g1q(irk_ctx *c, const P &prob, EnsArgs &a, char *ws, cudaStream_t st) {
+    return launch_queue(c, irk::ens_g1q_kernel<P>, irk::G1_THREADS, irk::G1_THREADS, &c->g1q_blocks_per_sm, a, ws, st,
+                        [&](const EnsArgs &aa, const irk::QueueArgs &qa, unsigned nb) {
+                            irk::ens_g1q_kernel<P><<<nb, irk::G1_THREADS, 0, st>>>(aa, qa, prob);
+                        });
 }
 
 template <class P>
@@ -409,6 +417,11 @@ int launch_chain_t(irk_ctx *c, double *y, double t0, char *ws, double *energy, i
     constexpr int CPB = irk::CH_THREADS / 32;
     const int64_t blocks = (c->batch + CPB - 1) / CPB;
     const double beta = c->params[0];
+    if (c->schedule != 1)
+        return launch_queue(c, irk::ens_chain_q_kernel<SPL>, irk::CH_THREADS, CPB, &c->chain_blocks_per_sm[SPL], a, ws,
+                            st, [&](const EnsArgs &aa, const irk::QueueArgs &qa, unsigned nb) {
+                                irk::ens_chain_q_kernel<SPL><<<nb, irk::CH_THREADS, 0, st>>>(aa, qa, beta);
+                            });
     return run_chunks(c, a, ws, blocks, CPB, 1, st, [&](const EnsArgs &aa, int64_t nb) {
         irk::ens_chain_kernel<SPL><<<(unsigned)nb, irk::CH_THREADS, 0, st>>>(aa, beta);
     });

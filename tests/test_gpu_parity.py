@@ -271,6 +271,32 @@ def test_work_queue_schedule_bitwise(irk, orc):
     assert np.array_equal(outs[1][4][idx], orr["dhloc"], equal_nan=True)
 
 
+def test_work_queue_chain_bitwise(irk, orc):
+    """Warp-level work queue of the FPU chain kernel: more chains than resident
+    warps, units of 9 steps, energy samples and Delta H^loc across units; equal
+    to the chunked launches and to the oracle."""
+    w = wl.fpu_ensemble(batch=4100, nsteps=90)
+    outs = []
+    for sched, bal in ((1, 0), (2, 9)):
+        with irk.Integrator(w.problem, w.dim, w.h, w.nsteps, w.batch, w.params, energy_every=15,
+                            balance=bal, schedule=sched, local_energy=True) as ig:
+            Y = torch.tensor(w.y, dtype=torch.float64, device="cuda")
+            ws = ig.new_workspace()
+            E = torch.zeros((ig.n_energy(), w.batch), dtype=torch.float64, device="cuda")
+            it = torch.zeros(w.batch, dtype=torch.int64, device="cuda")
+            ig.integrate(Y, ws, energy=E, iters=it)
+            rc, st = ig.stats(ws)
+            outs.append((Y.cpu().numpy(), E.cpu().numpy(), it.cpu().numpy(), st,
+                         ig.local_energy_error(ws).cpu().numpy()))
+    assert np.array_equal(outs[0][0], outs[1][0]) and np.array_equal(outs[0][1], outs[1][1])
+    assert np.array_equal(outs[0][2], outs[1][2]) and outs[0][3] == outs[1][3]
+    assert np.array_equal(outs[0][4], outs[1][4])
+    idx = np.arange(0, w.batch, 517)
+    orr = orc.integrate(w.problem, w.y[:, idx], w.params, w.h, w.nsteps, energy_every=15, local_energy=True)
+    assert np.array_equal(outs[1][0][:, idx], orr["y"]) and np.array_equal(outs[1][1][:, idx], orr["energy"])
+    assert np.array_equal(outs[1][2][idx], orr["iters"]) and np.array_equal(outs[1][4][idx], orr["dhloc"])
+
+
 # ------------------------------------------------------------------ config 3
 def test_config3_six_body_ragged_energy(irk, orc):
     """Config-3 generator, ragged batch of 37 members, 3,000 steps, energy every

@@ -28,6 +28,7 @@ def build_all():
 
 CFG = int(os.environ.get("IRK_VARIANT_CONFIG", "2"))
 NSTEPS = int(os.environ.get("IRK_VARIANT_NSTEPS", "0"))
+SCHED = int(os.environ.get("IRK_VARIANT_SCHEDULE", "0"))
 
 
 def time_one(name):
@@ -38,7 +39,7 @@ os.environ['IRK_LIB_OVERRIDE'] = {lib!r}
 sys.path.insert(0, {ROOT!r})
 from paper_2511_03655_b200 import irk, workloads as wl
 w = wl.config({CFG}, **({{'nsteps': {NSTEPS}}} if {NSTEPS} else {{}}))
-ig = irk.Integrator(w.problem, w.dim, w.h, w.nsteps, w.batch, w.params)
+ig = irk.Integrator(w.problem, w.dim, w.h, w.nsteps, w.batch, w.params, schedule={SCHED})
 y0 = torch.tensor(w.y, device='cuda'); Y = torch.empty_like(y0); ws = ig.new_workspace()
 ts = []
 for r in range(4):
@@ -46,7 +47,7 @@ for r in range(4):
     e0 = torch.cuda.Event(enable_timing=True); e1 = torch.cuda.Event(enable_timing=True)
     e0.record(); ig.integrate(Y, ws); e1.record(); torch.cuda.synchronize()
     ts.append(e0.elapsed_time(e1))
-print({name!r}, 'ms', min(ts[1:]), ts)
+print({name!r}, 'sched', {SCHED}, 'ms', min(ts[1:]), ts)
 """
     r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True)
     print(r.stdout.strip() or r.stderr[-500:])
