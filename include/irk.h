@@ -62,7 +62,11 @@ enum irk_option {
     IRK_OPT_MODE = 1,         /* 0 = partitioned (default, Eq. IRK_FP2), 1 = first-order (Eq. IRK_FP) */
     IRK_OPT_MAX_ITERS = 2,    /* sweeps cap per step, default 100 (flagged, step accepted)   */
     IRK_OPT_ENERGY_EVERY = 3, /* E > 0: sample H(y_n) at local steps 0, E, 2E, ... (default 0) */
-    IRK_OPT_MAPPING = 4,      /* 0 = auto; see DESIGN.md for the per-problem kernels          */
+    IRK_OPT_MAPPING = 4,      /* Kepler / Henon-Heiles (partitioned mode): IRK_MAP_AUTO (default),
+                                 IRK_MAP_G1 = one trajectory per thread, IRK_MAP_G8 = 8 lanes per
+                                 trajectory, one stage per lane (warp-shuffle contractions and
+                                 convergence reduction).  Other problems have one kernel each
+                                 (DESIGN.md "Mappings").  Bitwise-neutral.                     */
     IRK_OPT_BALANCE = 5,      /* ensemble scheduling: -1 = auto (default), 0 = off, C > 0 = run the
                                  call in chunks of C steps, re-sorting trajectories by the cost of
                                  the previous chunk (bitwise-neutral)  */
@@ -77,6 +81,8 @@ enum irk_option {
                                  (Eq. DHlocmax) over each call, in-kernel; read it with
                                  irk_local_energy_error (ensemble problems only)                   */
 };
+
+enum irk_mapping { IRK_MAP_AUTO = 0, IRK_MAP_G1 = 1, IRK_MAP_G8 = 8 };
 
 /* Create a context for `batch` independent trajectories of `problem` in
  * dimension `dim`, step h (finite, != 0; negative allowed), nsteps >= 0 steps per

@@ -1,0 +1,224 @@
+// Ensemble kernel, mapping "g8" (stage-per-lane): one group of 8 lanes per
+// trajectory, lane s of a group owns stage s (4 trajectories per warp).  The
+// north star's alternative to one trajectory per thread (the paper's own SIMD
+// mapping puts the 8 stages in the 8 lanes of an AVX-512 register):
+//
+//   a2  Lq_s = hb_s V_s; the group all-gathers Lq_0..7 by warp shuffles and lane s
+//       forms its row Q_s = q + D(mu_s., Lq)                    Eq. IRK_FP2 l.1-2
+//   a5  Delta_l = max_s |Q_s - Q_s^old|: a 3-step xor-shuffle max over the group
+//       (on the int64 bit patterns, NaN dropped), stop test replicated in the
+//       8 lanes                                                  Eq. stopping
+//   a3  F_s = g(Q_s, t + c_s h): ONE right-hand side per lane       Eq. IRK_FP2 l.3
+//   a4  Lv_s = hb_s F_s, all-gathered; V_s = v + D(W_s., Lv), W = nu on the sweep
+//       that finishes a step (next step's nu-init), else mu      Eq. IRK_FP2 l.4-5
+//   a6  q += S(Lq), v += S(Lv) from the gathered stages (every lane keeps the
+//       replicated q, v), history row s <- Lv_s                   Eq. yn3
+//
+// The coefficient rows mu_s., nu_s. are read from shared memory.  Every lane
+// executes the canonical operation sequence of its stage, so results are
+// bitwise those of the oracle and of the g1 mapping.  Trade-off (DESIGN.md
+// "Mappings"): 8x the lanes per trajectory (latency hiding at small batch) for
+// 2 x 8d shuffled doubles per sweep and the replicated update; g1 wins when the
+// batch fills the GPU, g8 when it does not (IRK_OPT_MAPPING auto).
+#pragma once
+#include <cstdint>
+
+#include "ens_common.cuh"
+#include "fp64.cuh"
+
+namespace irk {
+
+constexpr int G8_THREADS = 64;  // 8 trajectories per block
+
+#ifndef G8_MAXREG
+#define G8_MAXREG 128  // config-2 generator, 2,000 steps, B = 2048: 80 regs 5.8 ms, 96: 5.2, 128: 4.7 (g1: 8.7)
+#endif
+
+template <class P>
+__global__ void __maxnreg__(G8_MAXREG) ens_g8_kernel(const __grid_constant__ EnsArgs a,
+                                                            const __grid_constant__ P prob) {
+    constexpr int d = P::d, D = 2 * d;
+    const unsigned FULL = 0xffffffffu;
+    const int64_t B = a.batch;
+    const int lane = threadIdx.x & 31, s = lane & 7, base = lane & ~7;
+    const int64_t b = ((int64_t)blockIdx.x * G8_THREADS + threadIdx.x) >> 3;  // trajectory of the group
+    const bool valid = b < B;
+    const int64_t bb = valid ? b : 0;
+
+    // Lane-dependent coefficients from shared memory, column-major [j][s] so that
+    // the 8 lanes of a group read 8 consecutive doubles (all groups of the warp
+    // the same ones); nu~ offset by 72 doubles to sit in other banks than mu~.
+    // (Kept in registers they were rematerialised from the constant bank with
+    // lane-divergent addresses: serialised LDC, ncu mio_throttle.)
+    __shared__ double sW[72 + 64], sHB[8], sC[8];
+    for (int e = threadIdx.x; e < 64; e += blockDim.x) {
+        sW[(e & 7) * 8 + (e >> 3)] = (&c_mu[0][0])[e];       // mu~[i][j] at [j][i]
+        sW[72 + (e & 7) * 8 + (e >> 3)] = (&c_nu[0][0])[e];
+    }
+    if (threadIdx.x < 8) {
+        sHB[threadIdx.x] = a.hb[threadIdx.x];
+        sC[threadIdx.x] = c_c[threadIdx.x];
+    }
+    __syncthreads();
+    const double *Mu = sW + s, *Nu = sW + 72 + s;  // coefficient (s, j) at [8 j]
+
+    double q[d], v[d];
+#pragma unroll
+    for (int l = 0; l < d; ++l) {
+        q[l] = a.y[l * B + bb];
+        v[l] = a.y[(d + l) * B + bb];
+    }
+    int64_t bad = a.stats[1 * B + bb];
+    const int64_t n0 = *a.n_done;
+    const bool sample = (a.energy != nullptr) && (a.energy_every > 0);
+    double hprev = 0.0, dhmax = 0.0;
+    if (valid && s == 0) {
+        if (sample && a.c0 == 0) a.energy[b] = prob.energy(q, v);
+        if (a.local_energy) hprev = prob.energy(q, v);
+    }
+    bool live = valid && bad == 0 && a.nsteps > 0;
+    if (valid && !live && s == 0) {
+        if (a.iters && a.c0 == 0) a.iters[b] = 0;
+        if (a.csweeps) a.csweeps[b] = 0;
+        if (a.local_energy && a.c0 == 0) a.stats[3 * B + b] = 0;
+    }
+
+    // a1: V_s = v + D(nu_s., H), H = the history rows of all 8 stages
+    double Vs[d];
+    {
+        double Hs[d];
+#pragma unroll
+        for (int l = 0; l < d; ++l) Hs[l] = live ? a.hist[((int64_t)s * D + d + l) * B + b] : 0.0;
+#pragma unroll
+        for (int l = 0; l < d; ++l) {
+            double acc = dmul(Nu[0], __shfl_sync(FULL, Hs[l], base));
+#pragma unroll
+            for (int j = 1; j < 8; ++j) acc = dfma(Nu[8 * j], __shfl_sync(FULL, Hs[l], base + j), acc);
+            Vs[l] = dadd(v[l], acc);
+        }
+    }
+    constexpr int64_t kInfBits = 0x7ff0000000000000LL;
+    int64_t m[d], p[d];
+    double Qold[d];
+#pragma unroll
+    for (int l = 0; l < d; ++l) {
+        m[l] = p[l] = kInfBits;
+        Qold[l] = 0.0;
+    }
+    int64_t n = 0, hits = 0, sweeps = 0;
+    int k = 0;
+    while (__any_sync(FULL, live)) {  // warp-uniform: every lane takes part in the shuffles
+        ++k;
+        // ---- a2 + a5 ----
+        double sLq[d], Qs[d];  // S(Lq) is formed on the fly (the gathered Lq die here)
+        bool stop = (k >= 2);
+        const double hb_s = sHB[s];
+#pragma unroll
+        for (int l = 0; l < d; ++l) {
+            const double lq = dmul(hb_s, Vs[l]);
+            double g = __shfl_sync(FULL, lq, base);
+            double acc = dmul(Mu[0], g);
+            sLq[l] = g;
+#pragma unroll
+            for (int j = 1; j < 8; ++j) {
+                g = __shfl_sync(FULL, lq, base + j);
+                acc = dfma(Mu[8 * j], g, acc);
+                sLq[l] = dadd(sLq[l], g);
+            }
+            Qs[l] = dadd(q[l], acc);
+            int64_t e = __double_as_longlong(dsub(Qs[l], Qold[l])) & 0x7fffffffffffffffLL;
+            e = (e > kInfBits) ? 0 : e;  // NaN-ignoring max (canonical left-to-right form)
+            Qold[l] = Qs[l];
+#pragma unroll
+            for (int off = 1; off < 8; off <<= 1) {
+                const int64_t o = __shfl_xor_sync(FULL, e, off);
+                e = (o > e) ? o : e;
+            }
+            if (k >= 2) {  // reading R2, on the bit patterns as in ens_g1q
+                const int64_t mn = (e < p[l]) ? e : p[l];
+                const bool ok = (e == 0) || (m[l] <= mn);
+                m[l] = (p[l] < m[l]) ? p[l] : m[l];
+                p[l] = e;
+                stop = stop && ok;
+            }
+        }
+        // ---- a3: one right-hand side per lane ----
+        const double tn1 = dadd(a.t0, dmul((double)(n0 + n), a.h));
+        const double ts = dadd(tn1, dmul(sC[s], a.h));
+        double Fs[d];
+        {
+            bool ok = true;
+            prob.template accel<false>(Qs, Fs, ts, ok);
+            if (!ok) prob.template accel<true>(Qs, Fs, ts, ok);  // exact slow path, same bits
+        }
+        // ---- a4 (first half): Lv, all-gather ----
+        double Lvg[8][d], Lvs[d];
+#pragma unroll
+        for (int l = 0; l < d; ++l) {
+            Lvs[l] = dmul(sHB[s], Fs[l]);
+#pragma unroll
+            for (int j = 0; j < 8; ++j) Lvg[j][l] = __shfl_sync(FULL, Lvs[l], base + j);
+        }
+        const bool fin = live && (stop || k >= a.max_iters);
+        if (fin) {  // ---- a6: update (replicated in the group), history, samples ----
+            bool finite = true;
+#pragma unroll
+            for (int l = 0; l < d; ++l) {
+                double sv = Lvg[0][l];
+#pragma unroll
+                for (int j = 1; j < 8; ++j) sv = dadd(sv, Lvg[j][l]);
+                q[l] = dadd(q[l], sLq[l]);
+                v[l] = dadd(v[l], sv);
+                finite = finite && isfinite(q[l]) && isfinite(v[l]);
+            }
+            ++n;
+            sweeps += k;
+            hits += stop ? 0 : 1;
+            k = 0;
+#pragma unroll
+            for (int l = 0; l < d; ++l) m[l] = p[l] = kInfBits;
+            if (s == 0) {
+                if (sample && ((a.c0 + n) % a.energy_every) == 0)
+                    a.energy[((a.c0 + n) / a.energy_every) * B + b] = prob.energy(q, v);
+                if (a.local_energy) dhloc_update(prob.energy(q, v), hprev, dhmax);
+            }
+            if (n == a.nsteps || !finite) {  // leave: history row s = Lv_s, q block zeroed (R-4)
+#pragma unroll
+                for (int l = 0; l < d; ++l) {
+                    a.hist[((int64_t)s * D + l) * B + b] = 0.0;
+                    a.hist[((int64_t)s * D + d + l) * B + b] = Lvs[l];
+                }
+                if (!finite) bad = n0 + n;
+                live = false;
+            }
+        }
+        // ---- a4 (second half) / next step's a1: V_s = v + D(W_s., Lv) ----
+        {
+            const double *W = fin ? Nu : Mu;
+#pragma unroll
+            for (int l = 0; l < d; ++l) {
+                double acc = dmul(W[0], Lvg[0][l]);
+#pragma unroll
+                for (int j = 1; j < 8; ++j) acc = dfma(W[8 * j], Lvg[j][l], acc);
+                Vs[l] = dadd(v[l], acc);
+            }
+        }
+    }
+    if (valid && s == 0) {
+#pragma unroll
+        for (int l = 0; l < d; ++l) {
+            a.y[l * B + b] = q[l];
+            a.y[(d + l) * B + b] = v[l];
+        }
+        if (a.nsteps > 0 && a.stats[1 * B + b] == 0) {
+            a.stats[0 * B + b] += hits;
+            a.stats[1 * B + b] = bad;
+            a.stats[2 * B + b] += sweeps;
+            if (a.iters) a.iters[b] = (a.c0 == 0) ? sweeps : a.iters[b] + sweeps;
+            if (a.csweeps) a.csweeps[b] = (int32_t)sweeps;
+            if (a.local_energy) dhloc_store(&a.stats[3 * B + b], a.c0 == 0, dhmax);
+        }
+    }
+}
+
+}  // namespace irk

@@ -12,6 +12,7 @@
 #include "../../include/irk.h"
 #include "balance.cuh"
 #include "ensemble_g1.cuh"
+#include "ensemble_g8.cuh"
 #include "ensemble_nbody.cuh"
 #include "ensemble_chain.cuh"
 #include "nbody_direct.cuh"
@@ -55,6 +56,7 @@ struct irk_ctx {
 namespace {
 
 constexpr size_t kHeader = 64;
+constexpr int64_t kG8AutoMaxBatch = 8192;  // IRK_OPT_MAPPING auto: g8 up to this batch
 
 int fail(irk_ctx *c, int code, const char *fmt, ...) {
     char buf[512];
@@ -382,11 +384,36 @@ int launch_g1q(irk_ctx *c, const P &prob, EnsArgs &a, char *ws, cudaStream_t st)
                         });
 }
 
+// Stage-per-lane mapping (ensemble_g8.cuh): one launch, one group of 8 lanes per trajectory.
+template <class P>
+int launch_g8(irk_ctx *c, const P &prob, EnsArgs &a, char *ws, cudaStream_t st) {
+    a.nsteps = c->nsteps;
+    a.c0 = 0;
+    a.csweeps = nullptr;
+    a.perm = nullptr;
+    a.nslots = c->batch;
+    const int64_t blocks = (c->batch * 8 + irk::G8_THREADS - 1) / irk::G8_THREADS;
+    irk::ens_g8_kernel<P><<<(unsigned)blocks, irk::G8_THREADS, 0, st>>>(a, prob);
+    int rc = cuda_check(c, cudaGetLastError(), "ens_g8 launch");
+    if (rc) return rc;
+    advance_n_kernel<<<1, 1, 0, st>>>(reinterpret_cast<int64_t *>(ws), c->nsteps);
+    return cuda_check(c, cudaGetLastError(), "advance_n launch");
+}
+
+// IRK_OPT_MAPPING auto for the per-thread problems: g8 while the batch leaves
+// most g1 lanes of the GPU empty (measured crossover).
+bool use_g8(const irk_ctx *c) {
+    if (c->mapping == IRK_MAP_G8) return true;
+    if (c->mapping == IRK_MAP_G1) return false;
+    return c->batch <= kG8AutoMaxBatch;
+}
+
 template <class P>
 int launch_g1(irk_ctx *c, const P &prob, double *y, double t0, char *ws, double *energy,
               int64_t *iters, cudaStream_t st) {
     EnsArgs a = ens_args(c, y, t0, ws, energy, iters);
     const int64_t blocks = (c->batch + irk::G1_THREADS - 1) / irk::G1_THREADS;
+    if (c->mode == 0 && use_g8(c)) return launch_g8(c, prob, a, ws, st);
     if (c->mode == 0 && c->schedule != 1) return launch_g1q(c, prob, a, ws, st);
     if (c->mode == 1)
         return run_chunks(c, a, ws, blocks, irk::G1_THREADS / 32, 32, st, [&](const EnsArgs &aa, int64_t nb) {
@@ -642,7 +669,10 @@ int irk_set_option(irk_ctx *c, int key, int64_t val) {
         c->schedule = (int)val;
         return IRK_OK;
     case IRK_OPT_MAPPING:
-        if (val < 0 || val > 1) return fail(c, IRK_E_ARG, "irk_set_option: MAPPING must be 0 (auto) or 1");
+        if (val != IRK_MAP_AUTO && val != IRK_MAP_G1 && val != IRK_MAP_G8)
+            return fail(c, IRK_E_ARG, "irk_set_option: MAPPING must be 0 (auto), 1 (g1) or 8 (g8)");
+        if (val == IRK_MAP_G8 && c->problem != IRK_KEPLER && c->problem != IRK_HENON_HEILES)
+            return fail(c, IRK_E_ARG, "irk_set_option: the g8 mapping is built for Kepler and Henon-Heiles");
         c->mapping = (int)val;
         return IRK_OK;
     }

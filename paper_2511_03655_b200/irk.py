@@ -17,6 +17,7 @@ OK, W_MAXITER, E_ARG, E_CUDA, E_DIVERGED, E_COMM, E_STATE = 0, 1, -1, -2, -3, -4
 OPT_MODE, OPT_MAX_ITERS, OPT_ENERGY_EVERY, OPT_MAPPING, OPT_BALANCE, OPT_VSHARDS = 1, 2, 3, 4, 5, 6
 OPT_LOCAL_ENERGY = 7
 OPT_SCHEDULE = 8
+MAP_AUTO, MAP_G1, MAP_G8 = 0, 1, 8  # IRK_OPT_MAPPING (include/irk.h)
 PARTITIONED, FIRST_ORDER = 0, 1
 
 _HERE = os.path.dirname(os.path.abspath(__file__))

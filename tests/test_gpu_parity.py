@@ -297,6 +297,47 @@ def test_work_queue_chain_bitwise(irk, orc):
     assert np.array_equal(outs[1][2][idx], orr["iters"]) and np.array_equal(outs[1][4][idx], orr["dhloc"])
 
 
+@pytest.mark.parametrize("which", ["kepler", "hh"])
+def test_g8_stage_per_lane_mapping(irk, orc, which):
+    """IRK_OPT_MAPPING = 8 (one stage per lane, warp-shuffle contractions and
+    Delta reduction): bitwise equal to the oracle and to g1 -- states, sweeps,
+    energy samples, Delta H^loc, a diverging trajectory, and two chained calls."""
+    if which == "kepler":
+        w = wl.kepler_ensemble(batch=203, nsteps=600)
+        y = w.y.copy()
+        y[:, 7] = [1e-200, 0.0, 0.0, 0.0]
+    else:
+        w = wl.henon_heiles(batch=77, nsteps=600)
+        y = w.y.copy()
+    outs = []
+    for mp in (8, 1):
+        with irk.Integrator(w.problem, w.dim, w.h, w.nsteps // 2, w.batch, w.params, energy_every=50,
+                            mapping=mp, local_energy=True) as ig:
+            Y = torch.tensor(y, dtype=torch.float64, device="cuda")
+            ws = ig.new_workspace()
+            E = torch.zeros((ig.n_energy(), w.batch), dtype=torch.float64, device="cuda")
+            it = torch.zeros(w.batch, dtype=torch.int64, device="cuda")
+            ig.integrate(Y, ws, energy=E, iters=it)
+            E1, it1, d1 = E.cpu().numpy().copy(), it.cpu().numpy().copy(), ig.local_energy_error(ws).cpu().numpy()
+            ig.integrate(Y, ws, energy=E, iters=it)
+            rc, st = ig.stats(ws)
+            outs.append((Y.cpu().numpy(), E1, E.cpu().numpy(), it1 + it.cpu().numpy(), d1,
+                         ig.local_energy_error(ws).cpu().numpy(), st))
+    for a_, b_ in zip(outs[0][:6], outs[1][:6]):
+        assert np.array_equal(a_, b_, equal_nan=True)
+    assert outs[0][6] == outs[1][6]
+    o1 = orc.integrate(w.problem, y, w.params, w.h, w.nsteps // 2, energy_every=50, local_energy=True)
+    o2 = orc.integrate(w.problem, o1["y"], w.params, w.h, w.nsteps // 2, energy_every=50, local_energy=True,
+                       n0=w.nsteps // 2, hist=o1["hist"])
+    g = outs[0]
+    assert np.array_equal(g[0], o2["y"], equal_nan=True)
+    assert np.array_equal(g[1], o1["energy"], equal_nan=True) and np.array_equal(g[2], o2["energy"], equal_nan=True)
+    ok = np.isfinite(o1["y"]).all(axis=0)  # the oracle has no frozen state across calls
+    assert np.array_equal(g[3][ok], (o1["iters"] + o2["iters"])[ok])
+    assert np.array_equal(g[4], o1["dhloc"], equal_nan=True)
+    assert np.array_equal(g[5][ok], o2["dhloc"][ok], equal_nan=True)
+
+
 # ------------------------------------------------------------------ config 3
 def test_config3_six_body_ragged_energy(irk, orc):
     """Config-3 generator, ragged batch of 37 members, 3,000 steps, energy every
