@@ -234,6 +234,7 @@ static int problem_check(int problem, int dim, int nparams, const double *params
     case ORC_KEPLER: return (dim == 4 && nparams >= 1) ? 0 : -1;
     case ORC_HENON_HEILES: return (dim == 4 && nparams >= 2) ? 0 : -1;
     case ORC_FPU_BETA: return (dim >= 2 && dim % 2 == 0 && nparams >= 1) ? 0 : -1;
+    case ORC_SCHWARZSCHILD: return (dim == 4 && nparams >= 3) ? 0 : -1;
     case ORC_NBODY:
     case ORC_NBODY_DIRECT: {
         if (dim % 6 != 0 || dim < 12) return -1;
@@ -364,6 +365,110 @@ int orc_accel(int problem, int dim, const double *params, int nparams, double t,
 }
 
 /* ------------------------------------------------------------------ */
+/* Canonical sin / cos and the Schwarzschild black-hole problem          */
+/* ------------------------------------------------------------------ */
+
+/* Taylor coefficients RN((-1)^k / (2k+1)!) (sin) and RN((-1)^k / (2k)!) (cos),
+ * computed once from the exact factorials in __float128. */
+static double SIN_C[9], COS_C[10];
+static int have_sc = 0;
+
+static void sincos_init(void) {
+#pragma omp critical(orc_sincos_init)
+    {
+        if (!have_sc) {
+            q128 fact = 1;
+            for (int n = 1; n <= 20; ++n) {
+                fact *= n;
+                if (n >= 3 && n % 2 == 1) SIN_C[(n - 3) / 2] = (double)((((n - 1) / 2) % 2 ? -1 : 1) / fact);
+                if (n >= 2 && n % 2 == 0) COS_C[(n - 2) / 2] = (double)(((n / 2) % 2 ? -1 : 1) / fact);
+            }
+            have_sc = 1;
+        }
+    }
+}
+
+void orc_sincos(double x, double *sn, double *cs) {
+    if (!have_sc) sincos_init();
+    /* x = k pi/2 + t, |t| <= pi/4: pi/2 = P1 + P2 + P3 (each RN of the remainder) */
+    const double TWO_OVER_PI = 0x1.45f306dc9c883p-1;
+    const double P1 = 0x1.921fb54442d18p+0, P2 = 0x1.1a62633145c07p-54, P3 = -0x1.f1976b7ed8fbcp-110;
+    double k = rint(x * TWO_OVER_PI);
+    double t = fma(-k, P1, x);
+    t = fma(-k, P2, t);
+    t = fma(-k, P3, t);
+    double z = t * t;
+    double ps = SIN_C[8];
+    for (int i = 7; i >= 0; --i) ps = fma(ps, z, SIN_C[i]);
+    double st = fma(t * z, ps, t);           /* t + t^3 (S3 + z (S5 + ...)) */
+    double pc = COS_C[9];
+    for (int i = 8; i >= 0; --i) pc = fma(pc, z, COS_C[i]);
+    double ct = fma(z, pc, 1.0);             /* 1 + z (C2 + z (C4 + ...)) */
+    int q = (int)((long long)k & 3);
+    switch (q) {
+    case 0: *sn = st; *cs = ct; break;
+    case 1: *sn = ct; *cs = -st; break;
+    case 2: *sn = -st; *cs = -ct; break;
+    default: *sn = -ct; *cs = st; break;
+    }
+}
+
+/* Hamilton's equations of Eq. Ham_SBH, y = (r, theta, p_r, p_theta),
+ * P = {E, L, beta}; f = 1 - 2/r, s = sin theta, A = L - (beta/2) r^2 s^2:
+ *   r'       =  dH/dp_r     = f p_r
+ *   theta'   =  dH/dp_theta = p_theta / r^2
+ *   p_r'     = -dH/dr       = -(p_r^2/r^2 + E^2/(r^2 f^2) - p_theta^2/r^3 - beta A/r - A^2/(r^3 s^2))
+ *   p_theta' = -dH/dtheta   = beta A cos/s + A^2 cos/(r^2 s^3)
+ * in the canonical operation order of CANON.md. */
+static void rhs_schwarzschild(const double *P, const double *y, double *f) {
+    const double E = P[0], L = P[1], beta = P[2];
+    const double r = y[0], th = y[1], pr = y[2], pth = y[3];
+    double s, c;
+    orc_sincos(th, &s, &c);
+    const double fr = 1.0 - 2.0 / r;
+    const double r2 = r * r, s2 = s * s;
+    const double A = L - (0.5 * beta) * (r2 * s2);
+    const double r3 = r2 * r;
+    const double t1 = (pr * pr) / r2;
+    const double t2 = (E * E) / (r2 * (fr * fr));
+    const double t3 = (pth * pth) / r3;
+    const double t4 = (beta * A) / r;
+    const double t5 = (A * A) / (r3 * s2);
+    f[0] = fr * pr;
+    f[1] = pth / r2;
+    f[2] = -((((t1 + t2) - t3) - t4) - t5);
+    f[3] = ((beta * A) * c) / s + ((A * A) * c) / (r2 * (s2 * s));
+}
+
+static double energy_schwarzschild(const double *P, const double *y) {
+    const double E = P[0], L = P[1], beta = P[2];
+    const double r = y[0], th = y[1], pr = y[2], pth = y[3];
+    double s, c;
+    orc_sincos(th, &s, &c);
+    const double fr = 1.0 - 2.0 / r;
+    const double r2 = r * r, s2 = s * s;
+    const double A = L - (0.5 * beta) * (r2 * s2);
+    neum_t n = {0.0, 0.0};
+    neum_add(&n, 0.5 * (fr * (pr * pr)));
+    neum_add(&n, -(0.5 * ((E * E) / fr)));
+    neum_add(&n, (pth * pth) / (2.0 * r2));
+    neum_add(&n, (A * A) / (2.0 * (r2 * s2)));
+    return neum_result(&n);
+}
+
+int orc_rhs(int problem, int dim, const double *params, int nparams, double t, const double *y, double *f) {
+    if (problem_check(problem, dim, nparams, params)) return -1;
+    if (problem == ORC_SCHWARZSCHILD) {
+        rhs_schwarzschild(params, y, f);
+        return 0;
+    }
+    const int d = dim / 2;
+    for (int l = 0; l < d; ++l) f[l] = y[d + l];
+    accel_any(problem, dim, params, t, y, f + d, 0);
+    return 0;
+}
+
+/* ------------------------------------------------------------------ */
 /* Energies (canonical term order, Neumaier sums; CANON.md)             */
 /* ------------------------------------------------------------------ */
 
@@ -423,6 +528,7 @@ double orc_energy(int problem, int dim, const double *P, int nparams, const doub
     }
     case ORC_NBODY:
     case ORC_NBODY_DIRECT: return energy_nbody(dim / 6, P, y);
+    case ORC_SCHWARZSCHILD: return energy_schwarzschild(P, y);
     }
     return NAN;
 }
@@ -523,9 +629,14 @@ static int step_first_order(const orc_cfg *cfg, const coef_t *K, double tn1, dou
     *capped = 0;
     for (;;) {
         ++k;
-        /* F_i = f(t_{n-1} + c_i h, Y_i^[k-1]) = (V_i, g(Q_i)) */
+        /* F_i = f(t_{n-1} + c_i h, Y_i^[k-1]): (V_i, g(Q_i)) for the second-order
+         * problems, Hamilton's equations for Eq. Ham_SBH */
         for (int i = 0; i < S8; ++i) {
             double ti = tn1 + K->c[i] * cfg->h;
+            if (cfg->problem == ORC_SCHWARZSCHILD) {
+                rhs_schwarzschild(cfg->params, &w->Y[i * D], &w->F[i * D]);
+                continue;
+            }
             for (int l = 0; l < d; ++l) w->F[i * D + l] = w->Y[i * D + d + l];
             accel_any(cfg->problem, D, cfg->params, ti, &w->Y[i * D], &w->F[i * D + d], par);
         }
@@ -564,6 +675,9 @@ int orc_integrate(const orc_cfg *cfg, double *y, double *hist, double *energy, i
         return -1;
     if (cfg->max_iters < 1 || (cfg->mode != ORC_MODE_PARTITIONED && cfg->mode != ORC_MODE_FIRST_ORDER))
         return -1;
+    /* Eq. Ham_SBH is not separable: only the first-order iteration applies */
+    if (cfg->problem == ORC_SCHWARZSCHILD && cfg->mode != ORC_MODE_FIRST_ORDER) return -1;
+    sincos_init();
     /* the s = 8 tableau is computed once per process (pure function of s) */
     static coef_t K8;
     static int have_K8 = 0;

@@ -25,6 +25,8 @@ extern "C" {
 #define ORC_FPU_BETA 3      /* FPU-beta chain, fixed ends, params {beta}           */
 #define ORC_HENON_HEILES 4  /* Listing 2, params {lambda, xi}         */
 #define ORC_NBODY_DIRECT 5  /* large-N direct sum, blocked j-order, {G, eps>0, m}  */
+#define ORC_SCHWARZSCHILD 6 /* Eq. Ham_SBH, y = (r, theta, p_r, p_theta),
+                               params {E, L, beta}; first-order mode only             */
 
 #define ORC_MODE_PARTITIONED 0 /* Eqs. IRK_init2 / IRK_FP2, P:L267-283 (default)   */
 #define ORC_MODE_FIRST_ORDER 1 /* Eqs. IRK_init / IRK_FP               */
@@ -61,6 +63,16 @@ int orc_stop_test(const double *delta, int k);
  * built from it) for one state.  q: d positions; out: d accelerations. */
 int orc_accel(int problem, int dim, const double *params, int nparams, double t,
               const double *q, double *a);
+
+/* Full first-order right-hand side f(t, y) of one state (dim components):
+ * (v, g(q,t)) for the second-order problems, Hamilton's equations for
+ * ORC_SCHWARZSCHILD. */
+int orc_rhs(int problem, int dim, const double *params, int nparams, double t, const double *y,
+            double *f);
+
+/* Canonical sine and cosine (CANON.md "Canonical sin/cos"): Cody-Waite reduction
+ * by pi/2 in three parts, Taylor polynomials of degree 19 / 20 on |t| <= pi/4. */
+void orc_sincos(double x, double *s, double *c);
 
 /* Hamiltonian of one state y (dim), Neumaier-compensated, canonical order. */
 double orc_energy(int problem, int dim, const double *params, int nparams, const double *y);

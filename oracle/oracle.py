@@ -22,7 +22,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 SRC = os.path.join(HERE, "irk_oracle.c")
 LIB = os.path.join(HERE, "build", "liboracle.so")
 
-KEPLER, NBODY, FPU_BETA, HENON_HEILES, NBODY_DIRECT = 1, 2, 3, 4, 5
+KEPLER, NBODY, FPU_BETA, HENON_HEILES, NBODY_DIRECT, SCHWARZSCHILD = 1, 2, 3, 4, 5, 6
 PARTITIONED, FIRST_ORDER = 0, 1
 
 # -O2 without vectorisation or contraction: every op is the one written (CANON.md)
@@ -65,6 +65,9 @@ def lib():
             l.orc_stop_test.argtypes = [dp, ctypes.c_int]
             l.orc_accel.argtypes = [ctypes.c_int, ctypes.c_int, dp, ctypes.c_int, ctypes.c_double, dp, dp]
             l.orc_energy.argtypes = [ctypes.c_int, ctypes.c_int, dp, ctypes.c_int, dp]
+            l.orc_rhs.argtypes = [ctypes.c_int, ctypes.c_int, dp, ctypes.c_int, ctypes.c_double, dp, dp]
+            l.orc_sincos.argtypes = [ctypes.c_double, dp, dp]
+            l.orc_sincos.restype = None
             l.orc_energy.restype = ctypes.c_double
             l.orc_integrate.argtypes = [ctypes.POINTER(_Cfg), dp, dp, dp, ip, ip]
             _lib = l
@@ -108,6 +111,21 @@ def accel(problem: int, dim: int, params, q, t: float = 0.0):
     if lib().orc_accel(problem, dim, _dp(p), len(p), t, _dp(q), _dp(a)):
         raise ValueError("orc_accel: bad problem/dim/params")
     return a
+
+
+def rhs(problem: int, dim: int, params, y, t: float = 0.0):
+    """Full first-order f(t, y) of one state (Hamilton's equations for SCHWARZSCHILD)."""
+    p = _f64(params); y = _f64(y); f = np.zeros(dim)
+    if lib().orc_rhs(problem, dim, _dp(p), len(p), t, _dp(y), _dp(f)):
+        raise ValueError("orc_rhs: bad problem/dim/params")
+    return f
+
+
+def sincos(x: float):
+    """The canonical (sin x, cos x) of CANON.md."""
+    s = np.zeros(1); c = np.zeros(1)
+    lib().orc_sincos(float(x), _dp(s), _dp(c))
+    return float(s[0]), float(c[0])
 
 
 def energy(problem: int, dim: int, params, y) -> float:

@@ -18,7 +18,7 @@ from dataclasses import dataclass, field
 
 import numpy as np
 
-KEPLER, NBODY, FPU_BETA, HENON_HEILES, NBODY_DIRECT = 1, 2, 3, 4, 5
+KEPLER, NBODY, FPU_BETA, HENON_HEILES, NBODY_DIRECT, SCHWARZSCHILD = 1, 2, 3, 4, 5, 6
 
 SEEDS = {1: 1, 2: 2, 3: 3, 4: 4, 5: 5}
 
@@ -171,6 +171,28 @@ def henon_heiles(batch: int = 1, lam: float = 1.0, xi: float = 0.0, h: float = 2
     if batch > 1:
         y[:, 1:] += 1e-2 * g.standard_normal((4, batch - 1))
     return Workload("henon_heiles", HENON_HEILES, 4, y, np.array([lam, xi]), h, nsteps)
+
+
+SBH_E, SBH_L, SBH_BETA = 0.995, 4.6, 8.9e-4
+
+
+def schwarzschild(batch: int = 1, nsteps: int = 10000, h: float = 16.0, seed: int = 7) -> Workload:
+    """Charged particle near a magnetised Schwarzschild black hole (Eq. Ham_SBH,
+    P:L508-518) with the paper's parameters E = 0.995, L = 4.6, beta = 8.9e-4
+    (P:L533).  y = (r, theta, p_r, p_theta).  Trajectory 0 is the paper's initial
+    condition theta = pi/2, p_r = 0, r = 11 (a regular orbit), p_theta > 0 from
+    H = -1/2; the others start at r = 11 (1 + 1e-3 N(0,1)), same rule.  h = 16 is
+    the paper's reference step; the paper does not state the time span."""
+    g = _rng(seed)
+    r = np.full(batch, 11.0)
+    if batch > 1:
+        r[1:] *= 1.0 + 1e-3 * g.standard_normal(batch - 1)
+    f = 1.0 - 2.0 / r
+    A = SBH_L - 0.5 * SBH_BETA * r * r          # theta = pi/2: sin = 1
+    # H = -1/2 at p_r = 0: p_theta^2/(2 r^2) = -1/2 + E^2/(2 f) - A^2/(2 r^2)
+    pth = r * np.sqrt(2.0 * (-0.5 + 0.5 * SBH_E ** 2 / f - A * A / (2 * r * r)))
+    y = np.stack([r, np.full(batch, math.pi / 2), np.zeros(batch), pth])
+    return Workload("schwarzschild", SCHWARZSCHILD, 4, y, np.array([SBH_E, SBH_L, SBH_BETA]), h, nsteps)
 
 
 def config(i: int, **kw) -> Workload:
