@@ -44,8 +44,12 @@ enum irk_problem {
                               params {G, eps, m_1..m_N}                                   */
     IRK_FPU_BETA = 3,      /* FPU-beta chain, fixed ends, dim = 2N; params {beta}            */
     IRK_HENON_HEILES = 4,  /* Listing 2, dim = 4; params {lambda, xi}          */
-    IRK_NBODY_DIRECT = 5   /* large-N direct sum, canonical blocked j-order, dim = 6N;
+    IRK_NBODY_DIRECT = 5,  /* large-N direct sum, canonical blocked j-order, dim = 6N;
                               params {G, eps > 0, m_1..m_N}; batch must be 1                */
+    IRK_SCHWARZSCHILD = 6  /* charged particle near a magnetised Schwarzschild black hole,
+                              Eq. Ham_SBH, y = (r, theta, p_r, p_theta),
+                              dim = 4; params {E, L, beta}; not separable: first-order mode
+                              (set by irk_create, MODE = 0 rejected)                       */
 };
 
 enum irk_status {

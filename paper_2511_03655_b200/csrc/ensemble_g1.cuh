@@ -633,13 +633,20 @@ __global__ void __launch_bounds__(64) ens_g1fo_kernel(const __grid_constant__ En
             ++k;
 #pragma unroll
             for (int i = 0; i < 8; ++i) {
-                double F[d];
                 bool ok = true;
-                prob.template accel<true>(Y[i], F, dadd(tn1, dmul(c_c[i], a.h)), ok);
+                if constexpr (P::first_order) {  // f(y) of a non-separable problem
+                    double F[D];
+                    prob.template rhs<true>(Y[i], F, dadd(tn1, dmul(c_c[i], a.h)), ok);
 #pragma unroll
-                for (int l = 0; l < d; ++l) {
-                    L[i][l] = dmul(a.hb[i], Y[i][d + l]);
-                    L[i][d + l] = dmul(a.hb[i], F[l]);
+                    for (int l = 0; l < D; ++l) L[i][l] = dmul(a.hb[i], F[l]);
+                } else {                         // f(y) = (v, g(q, t))
+                    double F[d];
+                    prob.template accel<true>(Y[i], F, dadd(tn1, dmul(c_c[i], a.h)), ok);
+#pragma unroll
+                    for (int l = 0; l < d; ++l) {
+                        L[i][l] = dmul(a.hb[i], Y[i][d + l]);
+                        L[i][d + l] = dmul(a.hb[i], F[l]);
+                    }
                 }
             }
             stop = true;

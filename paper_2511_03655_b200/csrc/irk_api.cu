@@ -85,6 +85,7 @@ int n_params_expected(int problem, int dim) {
     case IRK_KEPLER: return 1;
     case IRK_HENON_HEILES: return 2;
     case IRK_FPU_BETA: return 1;
+    case IRK_SCHWARZSCHILD: return 3;
     case IRK_NBODY:
     case IRK_NBODY_DIRECT: return 2 + dim / 6;
     }
@@ -408,6 +409,17 @@ bool use_g8(const irk_ctx *c) {
     return c->batch <= kG8AutoMaxBatch;
 }
 
+// Non-separable first-order problems (P::first_order): the first-order kernel only.
+template <class P>
+int launch_first_order(irk_ctx *c, const P &prob, double *y, double t0, char *ws, double *energy, int64_t *iters,
+                       cudaStream_t st) {
+    EnsArgs a = ens_args(c, y, t0, ws, energy, iters);
+    const int64_t blocks = (c->batch + irk::G1_THREADS - 1) / irk::G1_THREADS;
+    return run_chunks(c, a, ws, blocks, irk::G1_THREADS / 32, 32, st, [&](const EnsArgs &aa, int64_t nb) {
+        irk::ens_g1fo_kernel<P><<<(unsigned)nb, irk::G1_THREADS, 0, st>>>(aa, prob);
+    });
+}
+
 template <class P>
 int launch_g1(irk_ctx *c, const P &prob, double *y, double t0, char *ws, double *energy,
               int64_t *iters, cudaStream_t st) {
@@ -583,6 +595,9 @@ irk_ctx *irk_create(int problem, int dim, double h, int64_t nsteps, int64_t batc
     case IRK_HENON_HEILES:
         if (dim != 4) return bad("irk_create: Kepler/Henon-Heiles need dim == 4");
         break;
+    case IRK_SCHWARZSCHILD:
+        if (dim != 4) return bad("irk_create: Schwarzschild needs dim == 4 (r, theta, p_r, p_theta)");
+        break;
     case IRK_FPU_BETA:
         if (dim < 2 || dim % 2) return bad("irk_create: FPU needs an even dim >= 2");
         if (dim / 2 != 32 && dim / 2 != 64 && dim / 2 != 128)
@@ -610,6 +625,7 @@ irk_ctx *irk_create(int problem, int dim, double h, int64_t nsteps, int64_t batc
     c->h = h;
     c->nsteps = nsteps;
     c->batch = batch;
+    if (problem == IRK_SCHWARZSCHILD) c->mode = 1;  // not separable: first-order iteration only
     char err[256];
     if (irk::build_tableau(h, &c->T, err, sizeof err)) {
         g_create_error = err;
@@ -637,8 +653,10 @@ int irk_set_option(irk_ctx *c, int key, int64_t val) {
     switch (key) {
     case IRK_OPT_MODE:
         if (val != 0 && val != 1) return fail(c, IRK_E_ARG, "irk_set_option: MODE must be 0 or 1");
-        if (val == 1 && c->problem != IRK_KEPLER && c->problem != IRK_HENON_HEILES)
-            return fail(c, IRK_E_ARG, "irk_set_option: first-order mode is built for Kepler and Henon-Heiles");
+        if (val == 1 && c->problem != IRK_KEPLER && c->problem != IRK_HENON_HEILES && c->problem != IRK_SCHWARZSCHILD)
+            return fail(c, IRK_E_ARG, "irk_set_option: first-order mode is built for Kepler, Henon-Heiles, Schwarzschild");
+        if (val == 0 && c->problem == IRK_SCHWARZSCHILD)
+            return fail(c, IRK_E_ARG, "irk_set_option: Schwarzschild is not separable (first-order mode only)");
         c->mode = (int)val;
         return IRK_OK;
     case IRK_OPT_MAX_ITERS:
@@ -704,6 +722,11 @@ int irk_integrate(irk_ctx *c, double *y, double t0, void *workspace, double *ene
     case IRK_HENON_HEILES: {
         irk::HenonHeiles P{c->params[0], c->params[1]};
         rc = launch_g1(c, P, y, t0, ws, energy, iters, st);
+        break;
+    }
+    case IRK_SCHWARZSCHILD: {
+        irk::Schwarzschild P{c->params[0], c->params[1], c->params[2]};
+        rc = launch_first_order(c, P, y, t0, ws, energy, iters, st);
         break;
     }
     case IRK_NBODY:
@@ -786,6 +809,10 @@ int irk_energy(irk_ctx *c, const double *y, double *H, void *stream) {
         break;
     case IRK_HENON_HEILES:
         energy_g1_kernel<<<blocks, threads, 0, st>>>(y, H, c->batch, irk::HenonHeiles{c->params[0], c->params[1]});
+        break;
+    case IRK_SCHWARZSCHILD:
+        energy_g1_kernel<<<blocks, threads, 0, st>>>(y, H, c->batch,
+                                                     irk::Schwarzschild{c->params[0], c->params[1], c->params[2]});
         break;
     case IRK_NBODY_DIRECT: {
         const int64_t N = c->dim / 6;

@@ -9,6 +9,7 @@ namespace irk {
 // Planar Kepler, H = |v|^2/2 - GM/|q| (the 2-body reduction of Eq. Ham2).
 struct Kepler {
     static constexpr int d = 2;
+    static constexpr bool first_order = false;  // g(q, t) of q'' = g: (v, g) in first-order mode
     double GM;
     // EXACT = false: branch-free fast paths, `ok` cleared if any needs the exact
     // intrinsic (the caller then re-evaluates with EXACT = true); same bits.
@@ -33,6 +34,7 @@ struct Kepler {
 // aux = lambda + xi sin(t); a1 = -q1 - 2 aux q1 q2; a2 = -q2 - aux (q1^2 - q2^2).
 struct HenonHeiles {
     static constexpr int d = 2;
+    static constexpr bool first_order = false;
     double lambda, xi;
     template <bool EXACT>
     __device__ __forceinline__ void accel(const double *q, double *a, double t, bool & /*ok*/) const {
@@ -49,6 +51,90 @@ struct HenonHeiles {
         n.add(dmul(0.5, dmul(q[1], q[1])));
         n.add(dmul(lambda, dmul(dmul(q[0], q[0]), q[1])));
         n.add(-dmul(lambda, ddiv(dmul(dmul(q[1], q[1]), q[1]), 3.0)));
+        return n.result();
+    }
+};
+
+// Canonical sine and cosine (oracle/CANON.md "Canonical sin / cos"): x = k pi/2 + t
+// by a three-part Cody-Waite reduction, Taylor polynomials of degree 19 / 20 in
+// t on |t| <= pi/4 (Horner in t^2 with fma), quadrant by k mod 4.  All
+// operations are IEEE-RN, so the result is the oracle's bit for bit (CUDA's own
+// sin/cos differ from libm in the last ulp).
+__device__ __forceinline__ void canon_sincos(double x, double &sn, double &cs) {
+    const double k = rint(dmul(x, 0x1.45f306dc9c883p-1));                    // RN(2/pi)
+    double t = dfma(-k, 0x1.921fb54442d18p+0, x);                            // pi/2 = P1 + P2 + P3
+    t = dfma(-k, 0x1.1a62633145c07p-54, t);
+    t = dfma(-k, -0x1.f1976b7ed8fbcp-110, t);
+    const double z = dmul(t, t);
+    // RN((-1)^j / (2j+1)!), j = 9 .. 1  and  RN((-1)^j / (2j)!), j = 10 .. 1
+    double ps = -0x1.2f49b46814157p-57;
+    ps = dfma(ps, z, 0x1.952c77030ad4ap-49);
+    ps = dfma(ps, z, -0x1.ae7f3e733b81fp-41);
+    ps = dfma(ps, z, 0x1.6124613a86d09p-33);
+    ps = dfma(ps, z, -0x1.ae64567f544e4p-26);
+    ps = dfma(ps, z, 0x1.71de3a556c734p-19);
+    ps = dfma(ps, z, -0x1.a01a01a01a01ap-13);
+    ps = dfma(ps, z, 0x1.1111111111111p-7);
+    ps = dfma(ps, z, -0x1.5555555555555p-3);
+    const double st = dfma(dmul(t, z), ps, t);
+    double pc = 0x1.e542ba4020225p-62;
+    pc = dfma(pc, z, -0x1.6827863b97d97p-53);
+    pc = dfma(pc, z, 0x1.ae7f3e733b81fp-45);
+    pc = dfma(pc, z, -0x1.93974a8c07c9dp-37);
+    pc = dfma(pc, z, 0x1.1eed8eff8d898p-29);
+    pc = dfma(pc, z, -0x1.27e4fb7789f5cp-22);
+    pc = dfma(pc, z, 0x1.a01a01a01a01ap-16);
+    pc = dfma(pc, z, -0x1.6c16c16c16c17p-10);
+    pc = dfma(pc, z, 0x1.5555555555555p-5);
+    pc = dfma(pc, z, -0.5);
+    const double ct = dfma(z, pc, 1.0);
+    switch ((int)((long long)k & 3)) {
+    case 0: sn = st; cs = ct; break;
+    case 1: sn = ct; cs = -st; break;
+    case 2: sn = -st; cs = -ct; break;
+    default: sn = -ct; cs = st; break;
+    }
+}
+
+// Charged particle near a magnetised Schwarzschild black hole, Eq. Ham_SBH
+// (P:L508-518), y = (r, theta | p_r, p_theta), parameters {E, L, beta}.
+// Not separable, so it is integrated in first-order mode only (Eqs. IRK_init /
+// IRK_FP): rhs() is Hamilton's equations in the canonical order of CANON.md.
+struct Schwarzschild {
+    static constexpr int d = 2;
+    static constexpr bool first_order = true;
+    double E, L, beta;
+    template <bool EXACT>
+    __device__ __forceinline__ void rhs(const double *y, double *f, double /*t*/, bool & /*ok*/) const {
+        const double r = y[0], pr = y[2], pth = y[3];
+        double s, c;
+        canon_sincos(y[1], s, c);
+        const double fr = dsub(1.0, ddiv(2.0, r));
+        const double r2 = dmul(r, r), s2 = dmul(s, s);
+        const double A = dsub(L, dmul(dmul(0.5, beta), dmul(r2, s2)));
+        const double r3 = dmul(r2, r);
+        const double t1 = ddiv(dmul(pr, pr), r2);
+        const double t2 = ddiv(dmul(E, E), dmul(r2, dmul(fr, fr)));
+        const double t3 = ddiv(dmul(pth, pth), r3);
+        const double t4 = ddiv(dmul(beta, A), r);
+        const double t5 = ddiv(dmul(A, A), dmul(r3, s2));
+        f[0] = dmul(fr, pr);
+        f[1] = ddiv(pth, r2);
+        f[2] = -dsub(dsub(dsub(dadd(t1, t2), t3), t4), t5);
+        f[3] = dadd(ddiv(dmul(dmul(beta, A), c), s), ddiv(dmul(dmul(A, A), c), dmul(r2, dmul(s2, s))));
+    }
+    __device__ __forceinline__ double energy(const double *q, const double *p) const {
+        const double r = q[0], pr = p[0], pth = p[1];
+        double s, c;
+        canon_sincos(q[1], s, c);
+        const double fr = dsub(1.0, ddiv(2.0, r));
+        const double r2 = dmul(r, r), s2 = dmul(s, s);
+        const double A = dsub(L, dmul(dmul(0.5, beta), dmul(r2, s2)));
+        Neumaier n;
+        n.add(dmul(0.5, dmul(fr, dmul(pr, pr))));
+        n.add(-dmul(0.5, ddiv(dmul(E, E), fr)));
+        n.add(ddiv(dmul(pth, pth), dmul(2.0, r2)));
+        n.add(ddiv(dmul(A, A), dmul(2.0, dmul(r2, s2))));
         return n.result();
     }
 };

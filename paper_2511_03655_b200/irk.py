@@ -12,7 +12,7 @@ import threading
 
 import numpy as np
 
-KEPLER, NBODY, FPU_BETA, HENON_HEILES, NBODY_DIRECT = 1, 2, 3, 4, 5
+KEPLER, NBODY, FPU_BETA, HENON_HEILES, NBODY_DIRECT, SCHWARZSCHILD = 1, 2, 3, 4, 5, 6
 OK, W_MAXITER, E_ARG, E_CUDA, E_DIVERGED, E_COMM, E_STATE = 0, 1, -1, -2, -3, -4, -5
 OPT_MODE, OPT_MAX_ITERS, OPT_ENERGY_EVERY, OPT_MAPPING, OPT_BALANCE, OPT_VSHARDS = 1, 2, 3, 4, 5, 6
 OPT_LOCAL_ENERGY = 7
@@ -93,7 +93,7 @@ class Integrator:
     """One irk_ctx.  y tensors are float64 (dim, batch), contiguous, on CUDA."""
 
     def __init__(self, problem: int, dim: int, h: float, nsteps: int, batch: int, params,
-                 *, mode: int = PARTITIONED, max_iters: int = 100, energy_every: int = 0,
+                 *, mode: int | None = None, max_iters: int = 100, energy_every: int = 0,
                  mapping: int = 0, balance: int = -1, vshards: int = 1, local_energy: bool = False,
                  schedule: int = 0):
         L = lib()
@@ -104,7 +104,9 @@ class Integrator:
         self.energy_every = energy_every
         p = np.ascontiguousarray(params, dtype=np.float64)
         self._check(L.irk_set_params(self._ctx, _dp(p), len(p)))
-        for key, val in ((OPT_MODE, mode), (OPT_MAX_ITERS, max_iters),
+        if mode is not None:  # default: the library's (partitioned; first-order for SCHWARZSCHILD)
+            self._check(L.irk_set_option(self._ctx, OPT_MODE, mode))
+        for key, val in ((OPT_MAX_ITERS, max_iters),
                          (OPT_ENERGY_EVERY, energy_every), (OPT_MAPPING, mapping),
                          (OPT_BALANCE, balance), (OPT_SCHEDULE, schedule)):
             self._check(L.irk_set_option(self._ctx, key, val))

@@ -338,6 +338,34 @@ def test_g8_stage_per_lane_mapping(irk, orc, which):
     assert np.array_equal(g[5][ok], o2["dhloc"][ok], equal_nan=True)
 
 
+def test_schwarzschild_first_order_parity(irk, orc):
+    """Eq. Ham_SBH (the paper's first-order problem) through the first-order
+    kernel: bitwise equal to the oracle (states, sweeps, energy samples, Delta
+    H^loc, the H entry point) on the paper's IC plus perturbed members; the
+    partitioned mode is rejected."""
+    w = wl.schwarzschild(batch=45, nsteps=600)
+    with irk.Integrator(w.problem, w.dim, w.h, w.nsteps, w.batch, w.params, energy_every=40,
+                        local_energy=True) as ig:
+        Y = torch.tensor(w.y, dtype=torch.float64, device="cuda")
+        ws = ig.new_workspace()
+        E = torch.zeros((ig.n_energy(), w.batch), dtype=torch.float64, device="cuda")
+        it = torch.zeros(w.batch, dtype=torch.int64, device="cuda")
+        ig.integrate(Y, ws, energy=E, iters=it)
+        rc, st = ig.stats(ws)
+        d = ig.local_energy_error(ws).cpu().numpy()
+        H = ig.energy(Y).cpu().numpy()
+        yg = Y.cpu().numpy()
+    o = orc.integrate(w.problem, w.y, w.params, w.h, w.nsteps, mode=orc.FIRST_ORDER, energy_every=40,
+                      local_energy=True)
+    assert rc == irk.OK
+    assert np.array_equal(yg, o["y"]) and np.array_equal(it.cpu().numpy(), o["iters"])
+    assert np.array_equal(E.cpu().numpy(), o["energy"]) and np.array_equal(d, o["dhloc"])
+    assert np.array_equal(H, [orc.energy(w.problem, 4, w.params, o["y"][:, b]) for b in range(w.batch)])
+    assert np.abs(o["energy"] + 0.5).max() < 1e-13
+    with pytest.raises(irk.IrkError):
+        irk.Integrator(w.problem, w.dim, w.h, w.nsteps, w.batch, w.params, mode=irk.PARTITIONED)
+
+
 # ------------------------------------------------------------------ config 3
 def test_config3_six_body_ragged_energy(irk, orc):
     """Config-3 generator, ragged batch of 37 members, 3,000 steps, energy every
