@@ -235,18 +235,21 @@ def test_cost_balanced_schedule_is_bitwise_neutral(irk, orc):
     assert np.array_equal(outs[1][2][idx], orr["iters"])
 
 
-def test_work_queue_schedule_bitwise(irk, orc):
+@pytest.mark.timeout(240)
+@pytest.mark.parametrize("unit", [7, 1])
+def test_work_queue_schedule_bitwise(irk, orc, unit):
     """The persistent work-queue launch (IRK_OPT_SCHEDULE = 2): more trajectories
-    than resident lanes, 17 units of 7 steps per trajectory (hand-offs between
-    lanes and SMs), energy samples and Delta H^loc straddling units, and two
-    trajectories that diverge mid-call.  Bitwise equal to the chunked launches
-    and to the oracle on a sample that includes the diverged trajectories."""
-    w = wl.kepler_ensemble(batch=70001, nsteps=119)
+    than resident lanes, units of 7 (or 1: every step a hand-off, maximal
+    parking of blocked units) steps, energy samples and Delta H^loc straddling
+    units, and two trajectories that diverge mid-call.  Bitwise equal to the
+    chunked launches and to the oracle on a sample that includes the diverged
+    trajectories."""
+    w = wl.kepler_ensemble(batch=70001, nsteps=119 if unit == 7 else 40)
     y = w.y.copy()
     y[:, 5] = [1e-200, 0.0, 0.0, 0.0]      # r = 0 -> non-finite at step 1
     y[:, 69990] = [1e-150, 0.0, 0.0, 1e-160]
     outs = []
-    for sched, bal in ((1, 0), (2, 7), (0, -1)):
+    for sched, bal in ((1, 0), (2, unit), (0, -1)):
         with irk.Integrator(w.problem, w.dim, w.h, w.nsteps, w.batch, w.params, energy_every=10,
                             balance=bal, schedule=sched, local_energy=True) as ig:
             Y = torch.tensor(y, dtype=torch.float64, device="cuda")
