@@ -113,37 +113,22 @@ __device__ __forceinline__ void nb_stage_accel(const double *Qi, int body, int l
 #endif
 constexpr int kNbRhsUnroll = NB_RHS_UNROLL;
 
+// One warp integrates its GPW trajectories (b = -1: idle group) over the
+// call-local steps [c0, c0 + nsteps).  Shared tiles belong to the calling block.
 template <int NB>
-__global__ void __maxnreg__(NB_MAXREG) ens_nbody_kernel(const __grid_constant__ EnsArgs a,
-                                                               const __grid_constant__ NBodyParams P) {
+__device__ __forceinline__ void nbody_unit(const EnsArgs &a, const NBodyParams &P, const int64_t b_in,
+                                           const int64_t c0, const int64_t nsteps, const double (*sW)[64],
+                                           double *sQ, double (*sQV)[6 * NB], const double *sm) {
     constexpr int GPW = 32 / NB;                 // groups (trajectories) per warp
-    constexpr int GPB = GPW * (NB_THREADS / 32);  // groups per block
     constexpr int d = 3 * NB, D = 6 * NB;
+    constexpr int GS = 8 * d + (((5 - 8 * d) % 16) + 16) % 16;
     const unsigned FULL = 0xffffffffu;
     const int64_t B = a.batch;
-
-    __shared__ __align__(16) double sW[2][64];         // mu~, nu~ for the per-group choice in a4
-    // Q^[k] of every body and stage (+ Q^[k-1] for Delta).  Group stride GS = 8d
-    // padded to 5 (mod 16) doubles: the 5 groups of a warp read the same
-    // relative offsets, which an unpadded 8d = 0 (mod 16) stride would put in one
-    // 64-bit bank (5-way conflicts; ncu: 2.7x the ideal shared wavefronts).
-    constexpr int GS = 8 * d + (((5 - 8 * d) % 16) + 16) % 16;
-    __shared__ double sQ[GPB * GS];
-    __shared__ double sQV[GPB][D];                      // (q, v) gathered for energy samples
-    __shared__ double sm[NB];
-    for (int e = threadIdx.x; e < 128; e += blockDim.x)
-        sW[e >> 6][e & 63] = (e < 64) ? (&c_mu[0][0])[e] : (&c_nu[0][0])[e - 64];
-    for (int e = threadIdx.x; e < NB; e += blockDim.x) sm[e] = P.m[e];
-    __syncthreads();
-
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int grp = lane / NB, body = lane % NB;
     const bool lane_ok = grp < GPW;
     const int gib = warp * GPW + (lane_ok ? grp : 0);   // group index inside the block
-    const int64_t slot = (int64_t)blockIdx.x * GPB + gib;
-    int64_t b = -1;
-    if (lane_ok && slot < a.nslots) b = a.perm ? (int64_t)a.perm[slot] : slot;
-    if (b >= B) b = -1;
+    const int64_t b = lane_ok ? b_in : -1;
     const bool valid = b >= 0;
     const unsigned gmask = lane_ok ? (((1u << NB) - 1u) << (grp * NB)) : 0u;
 
@@ -152,16 +137,16 @@ __global__ void __maxnreg__(NB_MAXREG) ens_nbody_kernel(const __grid_constant__ 
     if (valid) {
 #pragma unroll
         for (int c = 0; c < 3; ++c) {
-            q[c] = a.y[(int64_t)(3 * body + c) * B + b];
-            v[c] = a.y[(int64_t)(d + 3 * body + c) * B + b];
+            q[c] = __ldcg(&a.y[(int64_t)(3 * body + c) * B + b]);  // L2: may come from another SM
+            v[c] = __ldcg(&a.y[(int64_t)(d + 3 * body + c) * B + b]);
         }
-        bad = a.stats[1 * B + b];
+        bad = __ldcg(&a.stats[1 * B + b]);
     }
     const int64_t n0 = *a.n_done;
     const bool sample = (a.energy != nullptr) && (a.energy_every > 0);
     // energy at local step 0 (first chunk only); H(y) at the chunk start for DH^loc
     double hprev = 0.0, dhmax = 0.0;
-    if ((sample && a.c0 == 0) || a.local_energy) {
+    if ((sample && c0 == 0) || a.local_energy) {
         if (lane_ok) {
 #pragma unroll
             for (int c = 0; c < 3; ++c) {
@@ -172,13 +157,13 @@ __global__ void __maxnreg__(NB_MAXREG) ens_nbody_kernel(const __grid_constant__ 
         __syncwarp();
         if (valid && body == 0) {
             hprev = nbody_energy<NB>(sQV[gib], P);
-            if (sample && a.c0 == 0) a.energy[b] = hprev;
+            if (sample && c0 == 0) a.energy[b] = hprev;
         }
         __syncwarp();
     }
-    bool live = valid && bad == 0 && a.nsteps > 0;
+    bool live = valid && bad == 0 && nsteps > 0;
     if (valid && !live) {
-        if (a.iters && a.c0 == 0 && body == 0) a.iters[b] = 0;
+        if (a.iters && c0 == 0 && body == 0) a.iters[b] = 0;
         if (a.csweeps && body == 0) a.csweeps[b] = 0;
     }
 
@@ -193,7 +178,7 @@ __global__ void __maxnreg__(NB_MAXREG) ens_nbody_kernel(const __grid_constant__ 
 #pragma unroll
         for (int j = 0; j < 8; ++j)
 #pragma unroll
-            for (int c = 0; c < 3; ++c) H[j][c] = a.hist[((int64_t)j * D + d + 3 * body + c) * B + b];
+            for (int c = 0; c < 3; ++c) H[j][c] = __ldcg(&a.hist[((int64_t)j * D + d + 3 * body + c) * B + b]);
 #pragma unroll
         for (int i = 0; i < 8; ++i)
 #pragma unroll
@@ -306,7 +291,7 @@ __global__ void __maxnreg__(NB_MAXREG) ens_nbody_kernel(const __grid_constant__ 
         }
         const unsigned nonfinite = __ballot_sync(FULL, fin && !finite);
         const bool grp_bad = fin && ((nonfinite & gmask) != 0u);
-        const bool due = fin && sample && ((a.c0 + n) % a.energy_every) == 0;
+        const bool due = fin && sample && ((c0 + n) % a.energy_every) == 0;
         const bool need = due || (fin && a.local_energy);
         if (__any_sync(FULL, need)) {
             if (need) {
@@ -319,12 +304,12 @@ __global__ void __maxnreg__(NB_MAXREG) ens_nbody_kernel(const __grid_constant__ 
             __syncwarp();
             if (need && body == 0) {
                 const double hn = nbody_energy<NB>(sQV[gib], P);
-                if (due) a.energy[((a.c0 + n) / a.energy_every) * B + b] = hn;
+                if (due) a.energy[((c0 + n) / a.energy_every) * B + b] = hn;
                 if (a.local_energy) dhloc_update(hn, hprev, dhmax);
             }
             __syncwarp();
         }
-        if (fin && (n == a.nsteps || grp_bad)) {  // leave: history = Lv (R-4), q block zeroed
+        if (fin && (n == nsteps || grp_bad)) {  // leave: history = Lv (R-4), q block zeroed
 #pragma unroll
             for (int j = 0; j < 8; ++j)
 #pragma unroll
@@ -369,18 +354,75 @@ __global__ void __maxnreg__(NB_MAXREG) ens_nbody_kernel(const __grid_constant__ 
             a.y[(int64_t)(d + 3 * body + c) * B + b] = v[c];
         }
         if (body == 0) {
-            if (a.nsteps > 0 && a.stats[1 * B + b] == 0) {
-                a.stats[0 * B + b] += hits;
+            if (nsteps > 0 && __ldcg(&a.stats[1 * B + b]) == 0) {
+                a.stats[0 * B + b] = __ldcg(&a.stats[0 * B + b]) + hits;
                 a.stats[1 * B + b] = bad;
-                a.stats[2 * B + b] += sweeps;
-                if (a.iters) a.iters[b] = (a.c0 == 0) ? sweeps : a.iters[b] + sweeps;
+                a.stats[2 * B + b] = __ldcg(&a.stats[2 * B + b]) + sweeps;
+                if (a.iters) a.iters[b] = (c0 == 0) ? sweeps : __ldcg(&a.iters[b]) + sweeps;
                 if (a.csweeps) a.csweeps[b] = (int32_t)sweeps;
-                if (a.local_energy) dhloc_store(&a.stats[3 * B + b], a.c0 == 0, dhmax);
-            } else if (a.local_energy && a.c0 == 0) {
+                if (a.local_energy) dhloc_store(&a.stats[3 * B + b], c0 == 0, dhmax);
+            } else if (a.local_energy && c0 == 0) {
                 a.stats[3 * B + b] = 0;
             }
         }
     }
 }
+
+#define NB_SHARED_TILES                                                                              \
+    constexpr int GPW = 32 / NB, GPB = GPW * (NB_THREADS / 32), d = 3 * NB;                          \
+    constexpr int GS = 8 * d + (((5 - 8 * d) % 16) + 16) % 16;                                        \
+    __shared__ __align__(16) double sW[2][64];  /* mu~, nu~ for the per-group choice in a4 */          \
+    __shared__ double sQ[GPB * GS];             /* Q^[k] (+ Q^[k-1] for Delta), padded stride GS */     \
+    __shared__ double sQV[GPB][6 * NB];         /* (q, v) gathered for energy samples */               \
+    __shared__ double sm[NB];                                                                          \
+    for (int e = threadIdx.x; e < 128; e += blockDim.x)                                                \
+        sW[e >> 6][e & 63] = (e < 64) ? (&c_mu[0][0])[e] : (&c_nu[0][0])[e - 64];                      \
+    for (int e = threadIdx.x; e < NB; e += blockDim.x) sm[e] = P.m[e];                                 \
+    __syncthreads();
+
+// Chunked launch (IRK_OPT_SCHEDULE = 1): one warp per GPW slots of the (cost-sorted) order.
+template <int NB>
+__global__ void __maxnreg__(NB_MAXREG) ens_nbody_kernel(const __grid_constant__ EnsArgs a,
+                                                       const __grid_constant__ NBodyParams P) {
+    NB_SHARED_TILES
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int grp = lane / NB;
+    const int64_t slot = (int64_t)blockIdx.x * GPB + warp * GPW + (grp < GPW ? grp : 0);
+    int64_t b = -1;
+    if (grp < GPW && slot < a.nslots) b = a.perm ? (int64_t)a.perm[slot] : slot;
+    if (b >= a.batch) b = -1;
+    nbody_unit<NB>(a, P, b, a.c0, a.nsteps, sW, sQ, sQV, sm);
+}
+
+// Persistent warp-level work queue (IRK_OPT_SCHEDULE auto / 2): a unit is (warp
+// slot w = trajectories w*GPW .. w*GPW + GPW - 1, step chunk c); unit (w, c) waits
+// for progress[w] = c.  Same arithmetic per unit: bitwise any schedule.
+template <int NB>
+__global__ void __maxnreg__(NB_MAXREG) ens_nbody_q_kernel(const __grid_constant__ EnsArgs a,
+                                                         const __grid_constant__ QueueArgs qa,
+                                                         const __grid_constant__ NBodyParams P) {
+    NB_SHARED_TILES
+    const int lane = threadIdx.x & 31;
+    const int grp = lane / NB;
+    const int64_t W = (a.batch + GPW - 1) / GPW, total = W * qa.nchunks;
+    for (;;) {
+        unsigned long long u = 0;
+        if (lane == 0) u = atomicAdd(qa.counter, 1ull);
+        u = __shfl_sync(0xffffffffu, u, 0);
+        if ((int64_t)u >= total) break;
+        const int64_t c = (int64_t)u / W, w = (int64_t)u - c * W;
+        if (lane == 0 && c > 0)
+            while (ld_acquire(&qa.progress[w]) < c) __nanosleep(1024);
+        __syncwarp();
+        int64_t b = (grp < GPW) ? w * GPW + grp : -1;
+        if (b >= a.batch) b = -1;
+        const int64_t c0 = c * qa.qchunk;
+        nbody_unit<NB>(a, P, b, c0, (a.nsteps - c0 < qa.qchunk) ? a.nsteps - c0 : qa.qchunk, sW, sQ, sQV, sm);
+        __threadfence();  // this warp's stores of the unit, before the hand-off
+        __syncwarp();
+        if (lane == 0) st_release(&qa.progress[w], (int32_t)(c + 1));
+    }
+}
+#undef NB_SHARED_TILES
 
 }  // namespace irk

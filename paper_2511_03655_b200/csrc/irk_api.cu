@@ -35,6 +35,7 @@ struct irk_ctx {
     int schedule = 0;      // IRK_OPT_SCHEDULE: 0 auto, 1 chunked launches, 2 persistent work queue
     int g1q_blocks_per_sm = 0;  // occupancy of the work-queue kernels (queried once)
     int chain_blocks_per_sm[5] = {0, 0, 0, 0, 0};
+    int nbody_blocks_per_sm[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
     int local_energy = 0;  // IRK_OPT_LOCAL_ENERGY
     int64_t energy_every = 0;
     Tableau T;
@@ -445,6 +446,11 @@ int launch_nbody_t(irk_ctx *c, double *y, double t0, char *ws, double *energy, i
     EnsArgs a = ens_args(c, y, t0, ws, energy, iters);
     constexpr int GPW = 32 / NB, WPB = irk::NB_THREADS / 32;
     const int64_t blocks = (c->batch + GPW * WPB - 1) / (GPW * WPB);
+    if (c->schedule != 1)
+        return launch_queue(c, irk::ens_nbody_q_kernel<NB>, irk::NB_THREADS, GPW * WPB, &c->nbody_blocks_per_sm[NB], a,
+                            ws, st, [&](const EnsArgs &aa, const irk::QueueArgs &qa, unsigned nb) {
+                                irk::ens_nbody_q_kernel<NB><<<nb, irk::NB_THREADS, 0, st>>>(aa, qa, P);
+                            });
     return run_chunks(c, a, ws, blocks, WPB, GPW, st, [&](const EnsArgs &aa, int64_t nb) {
         irk::ens_nbody_kernel<NB><<<(unsigned)nb, irk::NB_THREADS, 0, st>>>(aa, P);
     });

@@ -369,6 +369,33 @@ def test_schwarzschild_first_order_parity(irk, orc):
         irk.Integrator(w.problem, w.dim, w.h, w.nsteps, w.batch, w.params, mode=irk.PARTITIONED)
 
 
+def test_work_queue_nbody_bitwise(irk, orc):
+    """Warp-level work queue of the body-per-lane kernel: a ragged batch (last
+    warp slot partly empty), more warp slots than resident warps, units of 13
+    steps, energy samples and Delta H^loc across units; equal to the chunked
+    launches and to the oracle."""
+    w = wl.six_body_ensemble(batch=9003, nsteps=130)
+    outs = []
+    for sched, bal in ((1, 0), (2, 13)):
+        with irk.Integrator(w.problem, w.dim, w.h, w.nsteps, w.batch, w.params, energy_every=26,
+                            balance=bal, schedule=sched, local_energy=True) as ig:
+            Y = torch.tensor(w.y, dtype=torch.float64, device="cuda")
+            ws = ig.new_workspace()
+            E = torch.zeros((ig.n_energy(), w.batch), dtype=torch.float64, device="cuda")
+            it = torch.zeros(w.batch, dtype=torch.int64, device="cuda")
+            ig.integrate(Y, ws, energy=E, iters=it)
+            rc, st = ig.stats(ws)
+            outs.append((Y.cpu().numpy(), E.cpu().numpy(), it.cpu().numpy(), st,
+                         ig.local_energy_error(ws).cpu().numpy()))
+    assert np.array_equal(outs[0][0], outs[1][0]) and np.array_equal(outs[0][1], outs[1][1])
+    assert np.array_equal(outs[0][2], outs[1][2]) and outs[0][3] == outs[1][3]
+    assert np.array_equal(outs[0][4], outs[1][4])
+    idx = np.r_[np.arange(0, w.batch, 1499), w.batch - 1]
+    orr = orc.integrate(w.problem, w.y[:, idx], w.params, w.h, w.nsteps, energy_every=26, local_energy=True)
+    assert np.array_equal(outs[1][0][:, idx], orr["y"]) and np.array_equal(outs[1][1][:, idx], orr["energy"])
+    assert np.array_equal(outs[1][2][idx], orr["iters"]) and np.array_equal(outs[1][4][idx], orr["dhloc"])
+
+
 # ------------------------------------------------------------------ config 3
 def test_config3_six_body_ragged_energy(irk, orc):
     """Config-3 generator, ragged batch of 37 members, 3,000 steps, energy every
