@@ -25,7 +25,10 @@
 
 namespace irk {
 
-constexpr int G1_THREADS = 64;
+#ifndef G1_BLOCK
+#define G1_BLOCK 64
+#endif
+constexpr int G1_THREADS = G1_BLOCK;
 #ifndef G1_MAXREG
 #define G1_MAXREG 168    // measured best on config 2 (tools/variants.py): 128: 116 ms, 144: 136, 168: 107, 190+: 109-111
 #endif
