@@ -81,6 +81,9 @@ enum irk_option {
                                  (trajectory, step-chunk) units from a work queue (per-thread
                                  problems, partitioned mode; BALANCE = C > 0 sets the unit length).
                                  Bitwise-neutral                          */
+    IRK_OPT_DEVICE_LOOP = 9,  /* IRK_NBODY_DIRECT: 1 (default) = the fixed-point sweeps run as a CUDA-graph
+                                 conditional WHILE loop on the device (one host sync per energy
+                                 sample / call); 0 = host loop, one sync per sweep               */
     IRK_OPT_LOCAL_ENERGY = 7  /* 1: track Delta H^loc_max = max_n |(H(y_n)-H(y_{n-1}))/H(y_{n-1})|
                                  (Eq. DHlocmax) over each call, in-kernel; read it with
                                  irk_local_energy_error (ensemble problems only)                   */
@@ -100,6 +103,12 @@ irk_ctx *irk_create(int problem, int dim, double h, int64_t nsteps, int64_t batc
 int irk_set_params(irk_ctx *ctx, const double *host_params, int n);
 
 int irk_set_option(irk_ctx *ctx, int key, int64_t val);
+
+/* Read an option (any IRK_OPT_*) or a read-only fact about the last call:
+ * IRK_INFO_DEVICE_LOOP_USED = 1 if the last IRK_NBODY_DIRECT call ran its sweeps as
+ * the device-side graph loop (0: host loop).  IRK_E_ARG for an unknown key. */
+enum irk_info { IRK_INFO_DEVICE_LOOP_USED = 100 };
+int irk_get_option(const irk_ctx *ctx, int key, int64_t *val);
 
 /* Bytes of caller-owned DEVICE workspace irk_integrate needs.  Layout: a
  * 64-byte header {int64 n_done, ...}, then the history L_{n-1} [8][dim][batch]

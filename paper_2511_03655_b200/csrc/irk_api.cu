@@ -2,6 +2,7 @@
 #include <cuda_runtime.h>
 
 #include <cmath>
+#include <cstddef>
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
@@ -51,6 +52,8 @@ struct irk_ctx {
     irk::NbdCtl *h_ctl = nullptr;  // pinned readback of the control block
     int nranks = 1, rank = 0;      // NCCL body sharding (irk_set_comm)
     int vshards = 1;               // virtual shards on one GPU (IRK_OPT_VSHARDS)
+    int device_loop = 1;           // IRK_OPT_DEVICE_LOOP (large-N path)
+    int device_loop_used = 0;      // IRK_INFO_DEVICE_LOOP_USED: the last call ran the graph loop
     void *nccl_comm = nullptr;
 };
 
@@ -298,20 +301,92 @@ int launch_direct(irk_ctx *c, double *y, double t0, char *ws, double *energy, in
     }
     for (int t = 0; t < nlocal; ++t) irk::nbd_init_kernel<<<cb, 128, 0, st>>>(A[t]);
     const dim3 fgrid((unsigned)((nloc + irk::NBD_FORCE_THREADS - 1) / irk::NBD_FORCE_THREADS), 8, (unsigned)nbd_nj(N));
+    // one fixed-point sweep of every local shard (a2+a5, exchange, a3, a4+a6, counters)
+    auto enqueue_sweep = [&](cudaStream_t s, cudaGraphConditionalHandle cond, int use_cond) -> int {
+        for (int t = 0; t < nlocal; ++t) irk::nbd_pos_kernel<<<cb, 128, 0, s>>>(A[t]);
+        if (nccl) {
+            int r = nccl_allgather_inplace(c, Qg, (size_t)stride, s);  // the exchange
+            if (r) return r;
+        }
+        irk::nbd_or_kernel<<<1, 1, 0, s>>>(A[0]);
+        for (int t = 0; t < nlocal; ++t) irk::nbd_force_kernel<<<fgrid, irk::NBD_FORCE_THREADS, 0, s>>>(A[t]);
+        for (int t = 0; t < nlocal; ++t) irk::nbd_vel_kernel<<<cb, 128, 0, s>>>(A[t]);
+        irk::nbd_ctl_kernel<<<1, 1, 0, s>>>(A[0], first, nlocal, n_done, stats, cond, use_cond);
+        return cuda_check(c, cudaGetLastError(), "direct sweep launch");
+    };
+    // Device-driven loop (IRK_OPT_DEVICE_LOOP, default on): the sweep captured once
+    // into the body of a CUDA-graph conditional WHILE node; nbd_ctl sets the
+    // condition, so the GPU runs sweep after sweep until n reaches the segment
+    // target (the next energy sample or nsteps) or the system diverges, and the
+    // host syncs once per segment instead of once per sweep.  Falls back to the
+    // host loop if the graph cannot be built (e.g. NCCL refusing capture).
+    cudaGraphExec_t gexec = nullptr;
+    if (c->device_loop) {
+        cudaGraph_t g = nullptr, body = nullptr;
+        cudaStream_t cs = nullptr;
+        cudaGraphConditionalHandle cond = 0;
+        bool okg = cudaGraphCreate(&g, 0) == cudaSuccess &&
+                   cudaGraphConditionalHandleCreate(&cond, g, 1, cudaGraphCondAssignDefault) == cudaSuccess;
+        if (okg) {
+            cudaGraphNodeParams cp = {};
+            cp.type = cudaGraphNodeTypeConditional;
+            cp.conditional.handle = cond;
+            cp.conditional.type = cudaGraphCondTypeWhile;
+            cp.conditional.size = 1;
+            cudaGraphNode_t node;
+            okg = cudaGraphAddNode(&node, g, nullptr, 0, &cp) == cudaSuccess;
+            if (okg) body = cp.conditional.phGraph_out[0];
+        }
+        okg = okg && cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking) == cudaSuccess &&
+              cudaStreamBeginCaptureToGraph(cs, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal) ==
+                  cudaSuccess;
+        if (okg) {
+            const int r = enqueue_sweep(cs, cond, 1);
+            cudaGraph_t captured = nullptr;
+            okg = (cudaStreamEndCapture(cs, &captured) == cudaSuccess) && r == IRK_OK &&
+                  cudaGraphInstantiate(&gexec, g, 0) == cudaSuccess;
+        }
+        if (!okg && gexec) {
+            cudaGraphExecDestroy(gexec);
+            gexec = nullptr;
+        }
+        if (cs) cudaStreamDestroy(cs);
+        if (g) cudaGraphDestroy(g);
+        cudaGetLastError();  // a failed attempt leaves no sticky error: use the host loop
+        c->err.clear();
+    }
     int64_t n = 0;
-    while (n < c->nsteps) {
-        for (int t = 0; t < nlocal; ++t) irk::nbd_pos_kernel<<<cb, 128, 0, st>>>(A[t]);
-        if (nccl && (rc = nccl_allgather_inplace(c, Qg, (size_t)stride, st))) return rc;  // the exchange
-        irk::nbd_or_kernel<<<1, 1, 0, st>>>(A[0]);
-        for (int t = 0; t < nlocal; ++t) irk::nbd_force_kernel<<<fgrid, irk::NBD_FORCE_THREADS, 0, st>>>(A[t]);
-        for (int t = 0; t < nlocal; ++t) irk::nbd_vel_kernel<<<cb, 128, 0, st>>>(A[t]);
-        irk::nbd_ctl_kernel<<<1, 1, 0, st>>>(A[0], first, nlocal, n_done, stats);
-        cudaMemcpyAsync(c->h_ctl, ctl, sizeof(irk::NbdCtl), cudaMemcpyDeviceToHost, st);
-        if ((rc = cuda_check(c, cudaStreamSynchronize(st), "direct sweep"))) return rc;
-        if (c->h_ctl->halt) break;
-        if (c->h_ctl->fin) {
+    c->device_loop_used = gexec ? 1 : 0;
+    if (gexec) {
+        while (n < c->nsteps) {
+            const int64_t target = (E > 0 && energy) ? ((n / E + 1) * E < c->nsteps ? (n / E + 1) * E : c->nsteps)
+                                                     : c->nsteps;
+            c->h_ctl->target = target;
+            cudaMemcpyAsync(&ctl->target, &c->h_ctl->target, sizeof(int64_t), cudaMemcpyHostToDevice, st);
+            cudaGraphLaunch(gexec, st);
+            cudaMemcpyAsync(c->h_ctl, ctl, offsetof(irk::NbdCtl, target), cudaMemcpyDeviceToHost, st);
+            if ((rc = cuda_check(c, cudaStreamSynchronize(st), "direct device loop"))) {
+                cudaGraphExecDestroy(gexec);
+                return rc;
+            }
+            if (c->h_ctl->halt) break;
             n = c->h_ctl->n;
-            if (E > 0 && energy && n % E == 0 && (rc = sample(n / E))) return rc;
+            if (E > 0 && energy && n % E == 0 && (rc = sample(n / E))) {
+                cudaGraphExecDestroy(gexec);
+                return rc;
+            }
+        }
+        cudaGraphExecDestroy(gexec);
+    } else {
+        while (n < c->nsteps) {
+            if ((rc = enqueue_sweep(st, 0, 0))) return rc;
+            cudaMemcpyAsync(c->h_ctl, ctl, sizeof(irk::NbdCtl), cudaMemcpyDeviceToHost, st);
+            if ((rc = cuda_check(c, cudaStreamSynchronize(st), "direct sweep"))) return rc;
+            if (c->h_ctl->halt) break;
+            if (c->h_ctl->fin) {
+                n = c->h_ctl->n;
+                if (E > 0 && energy && n % E == 0 && (rc = sample(n / E))) return rc;
+            }
         }
     }
     // final exchange: a divergence at the call's last step is recorded on every rank
@@ -688,6 +763,10 @@ int irk_set_option(irk_ctx *c, int key, int64_t val) {
             return fail(c, IRK_E_ARG, "irk_set_option: VSHARDS needs IRK_NBODY_DIRECT, N %% P == 0, no NCCL comm");
         c->vshards = (int)val;
         return IRK_OK;
+    case IRK_OPT_DEVICE_LOOP:
+        if (val != 0 && val != 1) return fail(c, IRK_E_ARG, "irk_set_option: DEVICE_LOOP must be 0 or 1");
+        c->device_loop = (int)val;
+        return IRK_OK;
     case IRK_OPT_SCHEDULE:
         if (val < 0 || val > 2) return fail(c, IRK_E_ARG, "irk_set_option: SCHEDULE must be 0, 1 or 2");
         c->schedule = (int)val;
@@ -701,6 +780,23 @@ int irk_set_option(irk_ctx *c, int key, int64_t val) {
         return IRK_OK;
     }
     return fail(c, IRK_E_ARG, "irk_set_option: unknown key %d", key);
+}
+
+int irk_get_option(const irk_ctx *c, int key, int64_t *val) {
+    if (!c || !val) return IRK_E_ARG;
+    switch (key) {
+    case IRK_OPT_MODE: *val = c->mode; return IRK_OK;
+    case IRK_OPT_MAX_ITERS: *val = c->max_iters; return IRK_OK;
+    case IRK_OPT_ENERGY_EVERY: *val = c->energy_every; return IRK_OK;
+    case IRK_OPT_MAPPING: *val = c->mapping; return IRK_OK;
+    case IRK_OPT_BALANCE: *val = c->balance; return IRK_OK;
+    case IRK_OPT_VSHARDS: *val = c->vshards; return IRK_OK;
+    case IRK_OPT_LOCAL_ENERGY: *val = c->local_energy; return IRK_OK;
+    case IRK_OPT_SCHEDULE: *val = c->schedule; return IRK_OK;
+    case IRK_OPT_DEVICE_LOOP: *val = c->device_loop; return IRK_OK;
+    case IRK_INFO_DEVICE_LOOP_USED: *val = c->device_loop_used; return IRK_OK;
+    }
+    return IRK_E_ARG;
 }
 
 size_t irk_workspace_bytes(const irk_ctx *c) {

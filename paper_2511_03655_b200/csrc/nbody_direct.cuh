@@ -45,6 +45,7 @@ struct NbdCtl {           // device-side control block (one per process)
     int32_t halt;         // stop integrating (divergence)
     int32_t pad;
     int64_t sweeps, hits;
+    int64_t target;       // device-driven loop: run sweeps until n == target (or halt)
 };
 
 // Per-shard arguments.  Component index l in [0, 3*nloc) of shard s is global
@@ -234,15 +235,18 @@ __global__ void nbd_vel_kernel(const __grid_constant__ NbdArgs a) {
     }
 }
 
-// after the last shard's nbd_vel of the sweep: counters, stats, reset local flags
+// after the last shard's nbd_vel of the sweep: counters, stats, reset local flags;
+// inside the device-driven loop (use_cond) also the WHILE condition of the graph
+// (no host round trip per fixed-point iteration)
 __global__ void nbd_ctl_kernel(const __grid_constant__ NbdArgs a, int first_local, int nlocal, int64_t *n_done,
-                               int64_t *stats) {
+                               int64_t *stats, cudaGraphConditionalHandle cond, int use_cond) {
     NbdCtl *c = a.ctl;
     for (int s = first_local; s < first_local + nlocal; ++s) nbd_slot(a, s)[nbd_flag_index(a)] = 0.0;
     if (c->nonfinite) {  // some shard diverged at the last completed step
         if (stats[1] == 0) stats[1] = *n_done;
         c->halt = 1;
         c->fin = 0;
+        if (use_cond) cudaGraphSetConditional(cond, 0);
         return;
     }
     const int k = c->k + 1;
@@ -261,6 +265,7 @@ __global__ void nbd_ctl_kernel(const __grid_constant__ NbdArgs a, int first_loca
     } else {
         c->k = k;
     }
+    if (use_cond) cudaGraphSetConditional(cond, (c->n < c->target) ? 1u : 0u);
 }
 
 // after the final exchange of a call: record a divergence at the last step

@@ -18,6 +18,8 @@ OPT_MODE, OPT_MAX_ITERS, OPT_ENERGY_EVERY, OPT_MAPPING, OPT_BALANCE, OPT_VSHARDS
 OPT_LOCAL_ENERGY = 7
 OPT_SCHEDULE = 8
 MAP_AUTO, MAP_G1, MAP_G8 = 0, 1, 8  # IRK_OPT_MAPPING (include/irk.h)
+OPT_DEVICE_LOOP = 9
+INFO_DEVICE_LOOP_USED = 100
 PARTITIONED, FIRST_ORDER = 0, 1
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
@@ -26,7 +28,7 @@ LIB_PATH = os.environ.get("IRK_LIB_OVERRIDE") or os.path.join(_HERE, "lib", "lib
 SYMBOLS = ["irk_create", "irk_set_params", "irk_set_option", "irk_workspace_bytes",
            "irk_integrate", "irk_integrate_host", "irk_energy", "irk_stats", "irk_tableau",
            "irk_set_comm", "irk_nccl_unique_id", "irk_last_error", "irk_destroy", "irk_probe_dfma",
-           "irk_probe_divsqrt", "irk_local_energy_error"]
+           "irk_probe_divsqrt", "irk_local_energy_error", "irk_get_option"]
 
 _lib = None
 _lock = threading.Lock()
@@ -68,6 +70,7 @@ def lib():
             l.irk_probe_dfma.restype = ctypes.c_int64
             l.irk_probe_divsqrt.argtypes = [vp, vp, vp, ctypes.c_int64, vp]
             l.irk_local_energy_error.argtypes = [vp, vp, vp, vp]
+            l.irk_get_option.argtypes = [vp, ctypes.c_int, i64p]
             _lib = l
     return _lib
 
@@ -95,7 +98,7 @@ class Integrator:
     def __init__(self, problem: int, dim: int, h: float, nsteps: int, batch: int, params,
                  *, mode: int | None = None, max_iters: int = 100, energy_every: int = 0,
                  mapping: int = 0, balance: int = -1, vshards: int = 1, local_energy: bool = False,
-                 schedule: int = 0):
+                 schedule: int = 0, device_loop: int = 1):
         L = lib()
         self._ctx = L.irk_create(problem, dim, h, nsteps, batch)
         if not self._ctx:
@@ -114,6 +117,8 @@ class Integrator:
             self._check(L.irk_set_option(self._ctx, OPT_VSHARDS, vshards))
         if local_energy:
             self._check(L.irk_set_option(self._ctx, OPT_LOCAL_ENERGY, 1))
+        if problem == NBODY_DIRECT:
+            self._check(L.irk_set_option(self._ctx, OPT_DEVICE_LOOP, device_loop))
         self.rank, self.nranks = 0, 1
 
     def set_comm(self, unique_id: bytes, rank: int, nranks: int):
@@ -198,6 +203,12 @@ class Integrator:
             self._check(rc)
         return rc, dict(maxiter_traj=int(out[0]), diverged_traj=int(out[1]),
                         first_bad_step=int(out[2]), total_sweeps=int(out[3]))
+
+    def get_option(self, key: int) -> int:
+        """irk_get_option: an IRK_OPT_* value or an IRK_INFO_* fact about the last call."""
+        out = np.zeros(1, dtype=np.int64)
+        self._check(lib().irk_get_option(self._ctx, key, out.ctypes.data_as(ctypes.POINTER(ctypes.c_int64))))
+        return int(out[0])
 
     def local_energy_error(self, workspace, stream=None):
         """Per-trajectory Delta H^loc_max of the last call (IRK_OPT_LOCAL_ENERGY)."""

@@ -514,6 +514,28 @@ def test_config5_full_size_first_steps(irk, orc):
     assert_parity(g, o, energy=True)
 
 
+@pytest.mark.parametrize("vshards", [1, 4])
+def test_config5_device_loop_equals_host_loop(irk, orc, vshards):
+    """IRK_OPT_DEVICE_LOOP: the sweeps of the large-N path as a CUDA-graph
+    conditional WHILE loop (segments end at energy samples) give the host-loop
+    and oracle results bit for bit, and the graph loop is what ran."""
+    w = wl.plummer(N=1024, nsteps=9)
+    o = orc.integrate(w.problem, w.y, w.params, w.h, w.nsteps, energy_every=4)
+    outs = []
+    for dl in (1, 0):
+        with irk.Integrator(w.problem, w.dim, w.h, w.nsteps, 1, w.params, energy_every=4, vshards=vshards,
+                            device_loop=dl) as ig:
+            Y = torch.tensor(w.y, dtype=torch.float64, device="cuda")
+            ws = ig.new_workspace()
+            E = torch.zeros((ig.n_energy(), 1), dtype=torch.float64, device="cuda")
+            it = torch.zeros(1, dtype=torch.int64, device="cuda")
+            ig.integrate(Y, ws, energy=E, iters=it)
+            assert ig.get_option(irk.INFO_DEVICE_LOOP_USED) == dl
+            outs.append((Y.cpu().numpy(), E.cpu().numpy(), int(it.item())))
+    for y, E, it in outs:
+        assert np.array_equal(y, o["y"]) and np.array_equal(E, o["energy"]) and it == int(o["iters"][0])
+
+
 # ---------------------------------------------------------- first-order mode
 def test_first_order_mode_parity(irk, orc):
     """IRK_OPT_MODE = 1 (Eqs. IRK_init / IRK_FP, stop test over all D from k = 1)
@@ -570,6 +592,7 @@ def test_config5_nccl_single_rank_path(irk, orc):
         ws = ig.new_workspace()
         E = torch.zeros((ig.n_energy(), 1), dtype=torch.float64, device="cuda")
         ig.integrate(Y, ws, energy=E)
+        print("NCCL path ran the device loop:", ig.get_option(irk.INFO_DEVICE_LOOP_USED))
         H = ig.energy(Y).cpu().numpy()
         assert np.array_equal(Y.cpu().numpy(), o["y"])
         assert np.array_equal(E.cpu().numpy(), o["energy"])
