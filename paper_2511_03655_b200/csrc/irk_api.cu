@@ -14,6 +14,7 @@
 #include "balance.cuh"
 #include "ensemble_g1.cuh"
 #include "ensemble_g8.cuh"
+#include "ensemble_fo.cuh"
 #include "ensemble_nbody.cuh"
 #include "ensemble_chain.cuh"
 #include "nbody_direct.cuh"
@@ -37,6 +38,7 @@ struct irk_ctx {
     int g1q_blocks_per_sm = 0;  // occupancy of the work-queue kernels (queried once)
     int chain_blocks_per_sm[5] = {0, 0, 0, 0, 0};
     int nbody_blocks_per_sm[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+    int fo_blocks_per_sm = 0;
     int local_energy = 0;  // IRK_OPT_LOCAL_ENERGY
     int64_t energy_every = 0;
     Tableau T;
@@ -485,11 +487,17 @@ bool use_g8(const irk_ctx *c) {
     return c->batch <= kG8AutoMaxBatch;
 }
 
-// Non-separable first-order problems (P::first_order): the first-order kernel only.
+// First-order mode (IRK_OPT_MODE = 1; the only mode of non-separable problems):
+// the sweep-granular work-queue kernel, or the chunked per-step kernel (SCHEDULE = 1).
 template <class P>
 int launch_first_order(irk_ctx *c, const P &prob, double *y, double t0, char *ws, double *energy, int64_t *iters,
                        cudaStream_t st) {
     EnsArgs a = ens_args(c, y, t0, ws, energy, iters);
+    if (c->schedule != 1)
+        return launch_queue(c, irk::ens_fo_q_kernel<P>, irk::FO_THREADS, irk::FO_THREADS, &c->fo_blocks_per_sm, a, ws, st,
+                            [&](const EnsArgs &aa, const irk::QueueArgs &qa, unsigned nb) {
+                                irk::ens_fo_q_kernel<P><<<nb, irk::FO_THREADS, 0, st>>>(aa, qa, prob);
+                            });
     const int64_t blocks = (c->batch + irk::G1_THREADS - 1) / irk::G1_THREADS;
     return run_chunks(c, a, ws, blocks, irk::G1_THREADS / 32, 32, st, [&](const EnsArgs &aa, int64_t nb) {
         irk::ens_g1fo_kernel<P><<<(unsigned)nb, irk::G1_THREADS, 0, st>>>(aa, prob);
@@ -503,10 +511,7 @@ int launch_g1(irk_ctx *c, const P &prob, double *y, double t0, char *ws, double 
     const int64_t blocks = (c->batch + irk::G1_THREADS - 1) / irk::G1_THREADS;
     if (c->mode == 0 && use_g8(c)) return launch_g8(c, prob, a, ws, st);
     if (c->mode == 0 && c->schedule != 1) return launch_g1q(c, prob, a, ws, st);
-    if (c->mode == 1)
-        return run_chunks(c, a, ws, blocks, irk::G1_THREADS / 32, 32, st, [&](const EnsArgs &aa, int64_t nb) {
-            irk::ens_g1fo_kernel<P><<<(unsigned)nb, irk::G1_THREADS, 0, st>>>(aa, prob);
-        });
+    if (c->mode == 1) return launch_first_order(c, prob, y, t0, ws, energy, iters, st);
     return run_chunks(c, a, ws, blocks, irk::G1_THREADS / 32, 32, st, [&](const EnsArgs &aa, int64_t nb) {
         irk::ens_g1_kernel<P><<<(unsigned)nb, irk::G1_THREADS, 0, st>>>(aa, prob);
     });

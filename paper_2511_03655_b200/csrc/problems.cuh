@@ -104,24 +104,27 @@ struct Schwarzschild {
     static constexpr int d = 2;
     static constexpr bool first_order = true;
     double E, L, beta;
+    // EXACT = false: branch-free division fast paths, `ok` cleared if any operand
+    // needs the exact intrinsic (the caller re-evaluates with EXACT = true); same bits.
     template <bool EXACT>
-    __device__ __forceinline__ void rhs(const double *y, double *f, double /*t*/, bool & /*ok*/) const {
+    __device__ __forceinline__ void rhs(const double *y, double *f, double /*t*/, bool &ok) const {
+        auto dv = [&ok](double num, double den) { return EXACT ? ddiv(num, den) : ddiv_fast(num, den, ok); };
         const double r = y[0], pr = y[2], pth = y[3];
         double s, c;
         canon_sincos(y[1], s, c);
-        const double fr = dsub(1.0, ddiv(2.0, r));
+        const double fr = dsub(1.0, dv(2.0, r));
         const double r2 = dmul(r, r), s2 = dmul(s, s);
         const double A = dsub(L, dmul(dmul(0.5, beta), dmul(r2, s2)));
         const double r3 = dmul(r2, r);
-        const double t1 = ddiv(dmul(pr, pr), r2);
-        const double t2 = ddiv(dmul(E, E), dmul(r2, dmul(fr, fr)));
-        const double t3 = ddiv(dmul(pth, pth), r3);
-        const double t4 = ddiv(dmul(beta, A), r);
-        const double t5 = ddiv(dmul(A, A), dmul(r3, s2));
+        const double t1 = dv(dmul(pr, pr), r2);
+        const double t2 = dv(dmul(E, E), dmul(r2, dmul(fr, fr)));
+        const double t3 = dv(dmul(pth, pth), r3);
+        const double t4 = dv(dmul(beta, A), r);
+        const double t5 = dv(dmul(A, A), dmul(r3, s2));
         f[0] = dmul(fr, pr);
-        f[1] = ddiv(pth, r2);
+        f[1] = dv(pth, r2);
         f[2] = -dsub(dsub(dsub(dadd(t1, t2), t3), t4), t5);
-        f[3] = dadd(ddiv(dmul(dmul(beta, A), c), s), ddiv(dmul(dmul(A, A), c), dmul(r2, dmul(s2, s))));
+        f[3] = dadd(dv(dmul(dmul(beta, A), c), s), dv(dmul(dmul(A, A), c), dmul(r2, dmul(s2, s))));
     }
     __device__ __forceinline__ double energy(const double *q, const double *p) const {
         const double r = q[0], pr = p[0], pth = p[1];
