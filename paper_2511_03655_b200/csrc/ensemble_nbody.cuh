@@ -105,6 +105,9 @@ __device__ __forceinline__ void nb_stage_accel(const double *Qi, int body, int l
     }
 }
 
+#ifndef NB_PHASED
+#define NB_PHASED 4  // RHS in groups of 8/NB_PHASED stages: weights, then shuffles, then sums (config 3, 5,000 steps: per-stage 219 ms, 4 groups 206)
+#endif
 #ifndef NB_MAXREG
 #define NB_MAXREG 168  // config 3, 5,000 steps: 168 -> 306 ms, 255 -> 309, 128 -> 342 (tools/variants.py)
 #endif
@@ -253,6 +256,52 @@ __device__ __forceinline__ void nbody_unit(const EnsArgs &a, const NBodyParams &
         const double tn1 = dadd(a.t0, dmul((double)(n0 + n), a.h));
         (void)tn1;  // the N-body RHS is autonomous
         bool okdiv = true;
+#if NB_PHASED
+        {   // phase-separated: all stages' own pair weights, then the shuffles, then the sums
+            constexpr int HF = NB / 2, HB = (NB - 1) / 2, SPH = 8 / NB_PHASED;  // stages per phase group
+#pragma unroll
+            for (int i0 = 0; i0 < 8; i0 += SPH) {
+            double wf[8][HF + 1], wb[8][HB + 1];
+#pragma unroll
+            for (int i = i0; i < i0 + SPH; ++i) {
+                const double *Qi = &sQ[gib * GS + i * d];
+                const double qx = Qi[3 * body], qy = Qi[3 * body + 1], qz = Qi[3 * body + 2];
+#pragma unroll
+                for (int o = 1; o <= HF; ++o) {
+                    const int j = (body + o < NB) ? body + o : body + o - NB;
+                    const double dx = dsub(Qi[3 * j], qx), dy = dsub(Qi[3 * j + 1], qy), dz = dsub(Qi[3 * j + 2], qz);
+                    const double r2 = dfma(dz, dz, dfma(dy, dy, dfma(dx, dx, P.eps2)));
+                    wf[i][o] = ddiv_fast(P.G, dmul(r2, dsqrt_fast(r2, okdiv)), okdiv);
+                }
+            }
+#pragma unroll
+            for (int i = i0; i < i0 + SPH; ++i)
+#pragma unroll
+                for (int o = 1; o <= HB; ++o) {
+                    const int src = lane - body + ((body - o >= 0) ? body - o : body - o + NB);
+                    wb[i][o] = __shfl_sync(FULL, wf[i][o], src & 31);
+                }
+#pragma unroll
+            for (int i = i0; i < i0 + SPH; ++i) {
+                const double *Qi = &sQ[gib * GS + i * d];
+                const double qx = Qi[3 * body], qy = Qi[3 * body + 1], qz = Qi[3 * body + 2];
+                double ax = 0.0, ay = 0.0, az = 0.0;
+#pragma unroll
+                for (int delta = 1; delta < NB; ++delta) {
+                    const int j = (body + delta < NB) ? body + delta : body + delta - NB;
+                    const double dx = dsub(Qi[3 * j], qx), dy = dsub(Qi[3 * j + 1], qy), dz = dsub(Qi[3 * j + 2], qz);
+                    const double s = dmul(sm[j], (delta <= HF) ? wf[i][delta] : wb[i][NB - delta]);
+                    ax = dfma(s, dx, ax);
+                    ay = dfma(s, dy, ay);
+                    az = dfma(s, dz, az);
+                }
+                Lv[i][0] = dmul(a.hb[i], ax);
+                Lv[i][1] = dmul(a.hb[i], ay);
+                Lv[i][2] = dmul(a.hb[i], az);
+            }
+            }
+        }
+#else
 #pragma unroll kNbRhsUnroll
         for (int i = 0; i < 8; ++i) {
             double ax, ay, az;
@@ -261,6 +310,7 @@ __device__ __forceinline__ void nbody_unit(const EnsArgs &a, const NBodyParams &
             Lv[i][1] = dmul(a.hb[i], ay);
             Lv[i][2] = dmul(a.hb[i], az);
         }
+#endif
         if (__any_sync(FULL, live && !okdiv)) {  // exact-intrinsic re-evaluation (same bits)
 #pragma unroll
             for (int i = 0; i < 8; ++i) {

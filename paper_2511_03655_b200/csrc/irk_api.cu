@@ -122,7 +122,12 @@ struct Sched {
     int32_t *perm, *csweeps, *sorted, *bins;
 };
 // thread-slot capacity of the scheduler's permutation (>= slots of any ensemble kernel)
-int64_t perm_slots(int64_t B) { return (B + 255) / 256 * 256; }  // >= slots of every mapping
+// >= the thread slots of every mapping: blocks x (warps x slots per warp) rounds B up
+// by less than one block (< 64 slots; e.g. ens_nbody: 10 slots per block, B = 16,384
+// -> 16,390 slots).  (Round 1 used round_up(B, 256), which the nbody mapping
+// overran into the csweeps array: a chunked, cost-sorted launch could then run a
+// trajectory in two groups at once.)
+int64_t perm_slots(int64_t B) { return (B + 64 + 255) / 256 * 256; }
 size_t sched_bytes(const irk_ctx *c) {
     return sizeof(int32_t) * ((size_t)perm_slots(c->batch) + 2 * (size_t)c->batch + irk::kCostBins);
 }

@@ -370,13 +370,14 @@ def test_schwarzschild_first_order_parity(irk, orc):
 
 
 def test_work_queue_nbody_bitwise(irk, orc):
-    """Warp-level work queue of the body-per-lane kernel: a ragged batch (last
-    warp slot partly empty), more warp slots than resident warps, units of 13
-    steps, energy samples and Delta H^loc across units; equal to the chunked
-    launches and to the oracle."""
-    w = wl.six_body_ensemble(batch=9003, nsteps=130)
+    """Warp-level work queue of the body-per-lane kernel (16,384 = 3,276 full warp
+    slots + a partial one), more warp slots than resident warps, units of 13
+    steps, energy samples and Delta H^loc across units; equal to the single
+    launch, to the chunked cost-sorted launches (whose permutation once overran
+    its buffer for this mapping) and to the oracle."""
+    w = wl.six_body_ensemble(batch=16384, nsteps=130)
     outs = []
-    for sched, bal in ((1, 0), (2, 13)):
+    for sched, bal in ((1, 0), (2, 13), (1, 26)):  # (1, 26): chunked + cost-sorted permutation
         with irk.Integrator(w.problem, w.dim, w.h, w.nsteps, w.batch, w.params, energy_every=26,
                             balance=bal, schedule=sched, local_energy=True) as ig:
             Y = torch.tensor(w.y, dtype=torch.float64, device="cuda")
@@ -387,9 +388,10 @@ def test_work_queue_nbody_bitwise(irk, orc):
             rc, st = ig.stats(ws)
             outs.append((Y.cpu().numpy(), E.cpu().numpy(), it.cpu().numpy(), st,
                          ig.local_energy_error(ws).cpu().numpy()))
-    assert np.array_equal(outs[0][0], outs[1][0]) and np.array_equal(outs[0][1], outs[1][1])
-    assert np.array_equal(outs[0][2], outs[1][2]) and outs[0][3] == outs[1][3]
-    assert np.array_equal(outs[0][4], outs[1][4])
+    for o in outs[1:]:
+        assert np.array_equal(outs[0][0], o[0]) and np.array_equal(outs[0][1], o[1])
+        assert np.array_equal(outs[0][2], o[2]) and outs[0][3] == o[3]
+        assert np.array_equal(outs[0][4], o[4])
     idx = np.r_[np.arange(0, w.batch, 1499), w.batch - 1]
     orr = orc.integrate(w.problem, w.y[:, idx], w.params, w.h, w.nsteps, energy_every=26, local_energy=True)
     assert np.array_equal(outs[1][0][:, idx], orr["y"]) and np.array_equal(outs[1][1][:, idx], orr["energy"])
