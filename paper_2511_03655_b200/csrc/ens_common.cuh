@@ -44,9 +44,22 @@ __device__ __forceinline__ void dhloc_update(double hn, double &hprev, double &d
 struct QueueArgs {
     unsigned long long *counter;  // next unit
     int32_t *progress;            // [batch] chunks completed in this call
+    int32_t *orphan;              // [batch] c > 0: unit (w, c) was fetched while blocked and parked
+                                  // for the warp finishing (w, c - 1); 0: none (ens_nbody_q)
     int64_t qchunk;               // steps per unit
     int64_t nchunks;              // units per trajectory
 };
+
+// Hand-off of a blocked unit.  Fetcher of (w, c), finding progress[w] < c: park it
+// (orphan[w]: 0 -> c), fence, re-read progress; if still < c the predecessor's
+// warp will run it, else reclaim it (orphan[w]: c -> 0).  Releaser of (w, c - 1):
+// publish progress[w] = c, fence, claim (orphan[w]: c -> 0).  With sequentially
+// consistent fences on both sides exactly one of the two runs the unit.
+__device__ __forceinline__ bool claim_orphan(const QueueArgs &qa, int32_t w, int64_t c) {
+    if (c >= qa.nchunks) return false;
+    __threadfence();
+    return atomicCAS(&qa.orphan[w], (int)c, 0) == (int)c;
+}
 
 // inter-unit hand-off of the work-queue kernels (gpu-scope release / acquire)
 __device__ __forceinline__ int32_t ld_acquire(const int32_t *p) {

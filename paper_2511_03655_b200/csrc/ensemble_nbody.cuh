@@ -455,14 +455,33 @@ __global__ void __maxnreg__(NB_MAXREG) ens_nbody_q_kernel(const __grid_constant_
     const int lane = threadIdx.x & 31;
     const int grp = lane / NB;
     const int64_t W = (a.batch + GPW - 1) / GPW, total = W * qa.nchunks;
+    int64_t c = 0, w = 0;
+    bool carry = false;  // continue slot w with unit c (parked for this warp by its fetcher)
     for (;;) {
-        unsigned long long u = 0;
-        if (lane == 0) u = atomicAdd(qa.counter, 1ull);
-        u = __shfl_sync(0xffffffffu, u, 0);
-        if ((int64_t)u >= total) break;
-        const int64_t c = (int64_t)u / W, w = (int64_t)u - c * W;
-        if (lane == 0 && c > 0)
-            while (ld_acquire(&qa.progress[w]) < c) __nanosleep(1024);
+        if (!carry) {
+            unsigned long long u = 0;
+            if (lane == 0) u = atomicAdd(qa.counter, 1ull);
+            u = __shfl_sync(0xffffffffu, u, 0);
+            if ((int64_t)u >= total) break;
+            c = (int64_t)u / W;
+            w = (int64_t)u - c * W;
+            // Predecessor (w, c - 1) still running: park the unit for the warp that
+            // runs it (hand-off protocol of ens_common.cuh) and fetch another one,
+            // rather than idling a warp for up to a whole unit.  Without this the
+            // queue fell into a convoy of waiting warps in some runs (config 3: 2.08
+            // or 2.85 s at random).
+            int go = 1;
+            if (lane == 0 && c > 0 && ld_acquire(&qa.progress[w]) < c) {
+                if (atomicCAS(&qa.orphan[w], 0, (int)c) == 0) {
+                    __threadfence();
+                    go = (ld_acquire(&qa.progress[w]) >= c && atomicCAS(&qa.orphan[w], (int)c, 0) == (int)c) ? 1 : 0;
+                } else {  // another unit of w already parked (rare): wait
+                    while (ld_acquire(&qa.progress[w]) < c) __nanosleep(1024);
+                }
+            }
+            go = __shfl_sync(0xffffffffu, go, 0);
+            if (!go) continue;
+        }
         __syncwarp();
         int64_t b = (grp < GPW) ? w * GPW + grp : -1;
         if (b >= a.batch) b = -1;
@@ -470,7 +489,13 @@ __global__ void __maxnreg__(NB_MAXREG) ens_nbody_q_kernel(const __grid_constant_
         nbody_unit<NB>(a, P, b, c0, (a.nsteps - c0 < qa.qchunk) ? a.nsteps - c0 : qa.qchunk, sW, sQ, sQV, sm);
         __threadfence();  // this warp's stores of the unit, before the hand-off
         __syncwarp();
-        if (lane == 0) st_release(&qa.progress[w], (int32_t)(c + 1));
+        int claimed = 0;
+        if (lane == 0) {
+            st_release(&qa.progress[w], (int32_t)(c + 1));
+            claimed = claim_orphan(qa, (int32_t)w, c + 1) ? 1 : 0;
+        }
+        carry = __shfl_sync(0xffffffffu, claimed, 0) != 0;
+        if (carry) ++c;
     }
 }
 #undef NB_SHARED_TILES
