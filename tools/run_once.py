@@ -14,6 +14,7 @@ ap.add_argument("--config", type=int, default=2)
 ap.add_argument("--batch", type=int, default=0)
 ap.add_argument("--nsteps", type=int, default=0)
 ap.add_argument("--reps", type=int, default=1)
+ap.add_argument("--host-loop", action="store_true", help="config 5: host-driven sweep loop (ncu sees each kernel)")
 a = ap.parse_args()
 kw = {}
 if a.batch:
@@ -21,7 +22,8 @@ if a.batch:
 if a.nsteps:
     kw["nsteps"] = a.nsteps
 w = wl.config(a.config, **kw)
-with irk.Integrator(w.problem, w.dim, w.h, w.nsteps, w.batch, w.params) as ig:
+kw2 = {"device_loop": 0} if (a.host_loop and w.problem == wl.NBODY_DIRECT) else {}
+with irk.Integrator(w.problem, w.dim, w.h, w.nsteps, w.batch, w.params, **kw2) as ig:
     y = torch.tensor(w.y, dtype=torch.float64, device="cuda")
     for _ in range(a.reps):
         ws = ig.new_workspace()
