@@ -58,7 +58,7 @@ def _stale() -> bool:
 
 
 def build(force: bool = False, verbose: bool = False, out: str | None = None,
-          defines: tuple = ()) -> str:
+          defines: tuple = (), extra_flags: tuple = ()) -> str:
     """Compile libirk.so (or, for A/B experiments, a variant with extra -D flags to `out`)."""
     lib_path = out or LIB
     if not force and out is None and not _stale():
@@ -76,7 +76,7 @@ def build(force: bool = False, verbose: bool = False, out: str | None = None,
     log = []
     for src in CU_SOURCES:
         o = os.path.join(bdir, src + ".o")
-        r = subprocess.run([nvcc, *NVCC_FLAGS, *[f"-D{x}" for x in defines], "-I", os.path.join(ROOT, "include"),
+        r = subprocess.run([nvcc, *NVCC_FLAGS, *extra_flags, *[f"-D{x}" for x in defines], "-I", os.path.join(ROOT, "include"),
                             "-I", _nccl_include(), "-c",
                             os.path.join(CSRC, src), "-o", o], capture_output=True, text=True)
         log.append(r.stdout + r.stderr)
