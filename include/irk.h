@@ -69,8 +69,9 @@ enum irk_option {
     IRK_OPT_MAPPING = 4,      /* Kepler / Henon-Heiles (partitioned mode): IRK_MAP_AUTO (default),
                                  IRK_MAP_G1 = one trajectory per thread, IRK_MAP_G8 = 8 lanes per
                                  trajectory, one stage per lane (warp-shuffle contractions and
-                                 convergence reduction).  Other problems have one kernel each
-                                 (DESIGN.md "Mappings").  Bitwise-neutral.                     */
+                                 convergence reduction).  IRK_NBODY: IRK_MAP_G1 = body per lane,
+                                 IRK_MAP_G8 = stage per lane (shared-memory all-gather).  Auto
+                                 picks by batch size.  Bitwise-neutral.  */
     IRK_OPT_BALANCE = 5,      /* ensemble scheduling: -1 = auto (default), 0 = off, C > 0 = run the
                                  call in chunks of C steps, re-sorting trajectories by the cost of
                                  the previous chunk (bitwise-neutral)  */

@@ -167,7 +167,8 @@ __device__ __forceinline__ void chain_unit(const EnsArgs &a, const double beta, 
                 ok_lane = ok_lane && oks;
             }
         }
-        const bool stop = (k >= 2) && __all_sync(FULL, ok_lane);
+        const bool all_ok = __all_sync(FULL, ok_lane);  // every lane votes (k is warp-uniform here)
+        const bool stop = (k >= 2) && all_ok;
         __syncwarp();
         // a3: bond forces of the lane's sites for every stage
         double Lv[8][SPL];

@@ -16,6 +16,7 @@
 #include "ensemble_g8.cuh"
 #include "ensemble_fo.cuh"
 #include "ensemble_nbody.cuh"
+#include "ensemble_nbody8.cuh"
 #include "ensemble_chain.cuh"
 #include "nbody_direct.cuh"
 #include "problems.cuh"
@@ -39,6 +40,7 @@ struct irk_ctx {
     int chain_blocks_per_sm[5] = {0, 0, 0, 0, 0};
     int nbody_blocks_per_sm[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
     int fo_blocks_per_sm = 0;
+    int nbody8_blocks_per_sm[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
     int local_energy = 0;  // IRK_OPT_LOCAL_ENERGY
     int64_t energy_every = 0;
     Tableau T;
@@ -62,7 +64,8 @@ struct irk_ctx {
 namespace {
 
 constexpr size_t kHeader = 64;
-constexpr int64_t kG8AutoMaxBatch = 8192;  // IRK_OPT_MAPPING auto: g8 up to this batch
+constexpr int64_t kG8AutoMaxBatch = 8192;  // IRK_OPT_MAPPING auto: g8 up to this batch (Kepler, HH)
+constexpr int64_t kN8AutoMaxBatch = 6144;  // IRK_OPT_MAPPING auto: stage-per-lane N-body up to this batch
 
 int fail(irk_ctx *c, int code, const char *fmt, ...) {
     char buf[512];
@@ -533,6 +536,15 @@ int launch_nbody_t(irk_ctx *c, double *y, double t0, char *ws, double *energy, i
     EnsArgs a = ens_args(c, y, t0, ws, energy, iters);
     constexpr int GPW = 32 / NB, WPB = irk::NB_THREADS / 32;
     const int64_t blocks = (c->batch + GPW * WPB - 1) / (GPW * WPB);
+    // stage-per-lane (ensemble_nbody8.cuh) when asked, or (auto) while the batch is too small to
+    // fill the GPU with body-per-lane groups (config-3 generator, 2,000 steps: 1.25x faster at
+    // 512-4,096 trajectories, equal at 8,192, 0.79x at 16,384)
+    if (c->mapping == IRK_MAP_G8 || (c->mapping == IRK_MAP_AUTO && c->batch <= kN8AutoMaxBatch))
+        return launch_queue(c, irk::ens_nbody8_kernel<NB>, irk::N8_THREADS, irk::N8_THREADS / 8,
+                            &c->nbody8_blocks_per_sm[NB], a, ws, st,
+                            [&](const EnsArgs &aa, const irk::QueueArgs &qa, unsigned nb) {
+                                irk::ens_nbody8_kernel<NB><<<nb, irk::N8_THREADS, 0, st>>>(aa, qa, P);
+                            });
     if (c->schedule != 1)
         return launch_queue(c, irk::ens_nbody_q_kernel<NB>, irk::NB_THREADS, GPW * WPB, &c->nbody_blocks_per_sm[NB], a,
                             ws, st, [&](const EnsArgs &aa, const irk::QueueArgs &qa, unsigned nb) {
@@ -786,8 +798,8 @@ int irk_set_option(irk_ctx *c, int key, int64_t val) {
     case IRK_OPT_MAPPING:
         if (val != IRK_MAP_AUTO && val != IRK_MAP_G1 && val != IRK_MAP_G8)
             return fail(c, IRK_E_ARG, "irk_set_option: MAPPING must be 0 (auto), 1 (g1) or 8 (g8)");
-        if (val == IRK_MAP_G8 && c->problem != IRK_KEPLER && c->problem != IRK_HENON_HEILES)
-            return fail(c, IRK_E_ARG, "irk_set_option: the g8 mapping is built for Kepler and Henon-Heiles");
+        if (val == IRK_MAP_G8 && c->problem != IRK_KEPLER && c->problem != IRK_HENON_HEILES && c->problem != IRK_NBODY)
+            return fail(c, IRK_E_ARG, "irk_set_option: the g8 mapping is built for Kepler, Henon-Heiles, N-body");
         c->mapping = (int)val;
         return IRK_OK;
     }

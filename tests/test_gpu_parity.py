@@ -398,6 +398,37 @@ def test_work_queue_nbody_bitwise(irk, orc):
     assert np.array_equal(outs[1][2][idx], orr["iters"]) and np.array_equal(outs[1][4][idx], orr["dhloc"])
 
 
+def test_nbody_stage_per_lane_mapping(irk, orc):
+    """IRK_NBODY with IRK_OPT_MAPPING = 8 (stage per lane, all pair weights of a
+    stage in one lane, shared-memory all-gather) equals the body-per-lane mapping
+    and the oracle bit for bit, over two chained calls with energy samples and
+    Delta H^loc, on a batch that leaves groups idle at the end of the queue."""
+    w = wl.six_body_ensemble(batch=601, nsteps=400)
+    outs = []
+    for mp in (8, 1):
+        with irk.Integrator(w.problem, w.dim, w.h, w.nsteps // 2, w.batch, w.params, energy_every=40,
+                            mapping=mp, local_energy=True) as ig:
+            Y = torch.tensor(w.y, dtype=torch.float64, device="cuda")
+            ws = ig.new_workspace()
+            E = torch.zeros((ig.n_energy(), w.batch), dtype=torch.float64, device="cuda")
+            it = torch.zeros(w.batch, dtype=torch.int64, device="cuda")
+            ig.integrate(Y, ws, energy=E, iters=it)
+            E1, it1 = E.cpu().numpy().copy(), it.cpu().numpy().copy()
+            ig.integrate(Y, ws, energy=E, iters=it)
+            outs.append((Y.cpu().numpy(), E1, E.cpu().numpy(), it1 + it.cpu().numpy(),
+                         ig.local_energy_error(ws).cpu().numpy(), ig.stats(ws)[1]))
+    for a_, b_ in zip(outs[0][:5], outs[1][:5]):
+        assert np.array_equal(a_, b_)
+    assert outs[0][5] == outs[1][5]
+    idx = np.arange(0, w.batch, 97)
+    o1 = orc.integrate(w.problem, w.y[:, idx], w.params, w.h, w.nsteps // 2, energy_every=40)
+    o2 = orc.integrate(w.problem, o1["y"], w.params, w.h, w.nsteps // 2, energy_every=40, local_energy=True,
+                       n0=w.nsteps // 2, hist=o1["hist"])
+    assert np.array_equal(outs[0][0][:, idx], o2["y"]) and np.array_equal(outs[0][2][:, idx], o2["energy"])
+    assert np.array_equal(outs[0][3][idx], o1["iters"] + o2["iters"])
+    assert np.array_equal(outs[0][4][idx], o2["dhloc"])
+
+
 # ------------------------------------------------------------------ config 3
 def test_config3_six_body_ragged_energy(irk, orc):
     """Config-3 generator, ragged batch of 37 members, 3,000 steps, energy every
