@@ -30,6 +30,9 @@ namespace irk {
 
 constexpr int G8_THREADS = 64;  // 8 trajectories per block
 
+#ifndef G8_SMEM
+#define G8_SMEM 1  // all-gathers through a shared-memory tile (0: shuffles; 2,000 steps at B = 512: 3.65 vs 4.65 ms)
+#endif
 #ifndef G8_MAXREG
 #define G8_MAXREG 128  // config-2 generator, 2,000 steps, B = 2048: 80 regs 5.8 ms, 96: 5.2, 128: 4.7 (g1: 8.7)
 #endif
@@ -51,6 +54,11 @@ __global__ void __maxnreg__(G8_MAXREG) ens_g8_kernel(const __grid_constant__ Ens
     // (Kept in registers they were rematerialised from the constant bank with
     // lane-divergent addresses: serialised LDC, ncu mio_throttle.)
     __shared__ double sW[72 + 64], sHB[8], sC[8];
+#if G8_SMEM
+    // per-group all-gather tile [stage][component], groups padded into different banks
+    __shared__ __align__(16) double sG[G8_THREADS / 8][8 * d + 2];
+    const int gib = threadIdx.x >> 3;
+#endif
     for (int e = threadIdx.x; e < 64; e += blockDim.x) {
         sW[(e & 7) * 8 + (e >> 3)] = (&c_mu[0][0])[e];       // mu~[i][j] at [j][i]
         sW[72 + (e & 7) * 8 + (e >> 3)] = (&c_nu[0][0])[e];
@@ -114,14 +122,26 @@ __global__ void __maxnreg__(G8_MAXREG) ens_g8_kernel(const __grid_constant__ Ens
         bool stop = (k >= 2);
         const double hb_s = sHB[s];
 #pragma unroll
+#if G8_SMEM
+        for (int l = 0; l < d; ++l) sG[gib][s * d + l] = dmul(hb_s, Vs[l]);
+        __syncwarp();
+#endif
         for (int l = 0; l < d; ++l) {
+#if G8_SMEM
+            double g = sG[gib][l];
+#else
             const double lq = dmul(hb_s, Vs[l]);
             double g = __shfl_sync(FULL, lq, base);
+#endif
             double acc = dmul(Mu[0], g);
             sLq[l] = g;
 #pragma unroll
             for (int j = 1; j < 8; ++j) {
+#if G8_SMEM
+                g = sG[gib][j * d + l];
+#else
                 g = __shfl_sync(FULL, lq, base + j);
+#endif
                 acc = dfma(Mu[8 * j], g, acc);
                 sLq[l] = dadd(sLq[l], g);
             }
@@ -153,12 +173,24 @@ __global__ void __maxnreg__(G8_MAXREG) ens_g8_kernel(const __grid_constant__ Ens
         }
         // ---- a4 (first half): Lv, all-gather ----
         double Lvg[8][d], Lvs[d];
+#if G8_SMEM
+        __syncwarp();  // the Lq reads of this sweep are done
+#pragma unroll
+        for (int l = 0; l < d; ++l) sG[gib][s * d + l] = Lvs[l] = dmul(sHB[s], Fs[l]);
+        __syncwarp();
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+#pragma unroll
+            for (int l = 0; l < d; ++l) Lvg[j][l] = sG[gib][j * d + l];
+        __syncwarp();  // before the next sweep's writes
+#else
 #pragma unroll
         for (int l = 0; l < d; ++l) {
             Lvs[l] = dmul(sHB[s], Fs[l]);
 #pragma unroll
             for (int j = 0; j < 8; ++j) Lvg[j][l] = __shfl_sync(FULL, Lvs[l], base + j);
         }
+#endif
         const bool fin = live && (stop || k >= a.max_iters);
         if (fin) {  // ---- a6: update (replicated in the group), history, samples ----
             bool finite = true;

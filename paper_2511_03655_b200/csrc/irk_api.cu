@@ -64,7 +64,7 @@ struct irk_ctx {
 namespace {
 
 constexpr size_t kHeader = 64;
-constexpr int64_t kG8AutoMaxBatch = 8192;  // IRK_OPT_MAPPING auto: g8 up to this batch (Kepler, HH)
+constexpr int64_t kG8AutoMaxBatch = 12288;  // IRK_OPT_MAPPING auto: g8 up to this batch (Kepler, HH)
 constexpr int64_t kN8AutoMaxBatch = 6144;  // IRK_OPT_MAPPING auto: stage-per-lane N-body up to this batch
 
 int fail(irk_ctx *c, int code, const char *fmt, ...) {
