@@ -236,3 +236,166 @@ __global__ void __maxnreg__(FO_MAXREG) ens_fo_q_kernel(const __grid_constant__ E
 }
 
 }  // namespace irk
+
+namespace irk {
+
+// First-order mode, stage per lane ("g8", small batches and single trajectories,
+// e.g. the paper's one-orbit Schwarzschild runs): a group of 8 lanes per
+// trajectory, lane s owns stage s -- Y_s (all D components) and its right-hand
+// side f(Y_s); L is all-gathered through a per-group shared-memory tile, every
+// lane forms Yn_s = y + D(mu_s., L), Delta_l = max over the 8 stages by an
+// xor-shuffle max, the stop test and y are replicated in the group.  On a
+// finished step the lane overwrites its discarded Yn_s with the next step's
+// nu-init.  Same canonical sequence as the oracle's step_first_order.
+constexpr int FO8_THREADS = 64;
+
+template <class P>
+__global__ void __maxnreg__(128) ens_fo8_kernel(const __grid_constant__ EnsArgs a, const __grid_constant__ P prob) {
+    constexpr int d = P::d, D = 2 * d;
+    const unsigned FULL = 0xffffffffu;
+    const int64_t B = a.batch;
+    const int lane = threadIdx.x & 31, s = lane & 7, gib = threadIdx.x >> 3;
+    const int64_t b = ((int64_t)blockIdx.x * FO8_THREADS + threadIdx.x) >> 3;
+    const bool valid = b < B;
+    const int64_t bb = valid ? b : 0;
+    __shared__ double sW[72 + 64], sHB[8], sC[8];
+    __shared__ __align__(16) double sG[FO8_THREADS / 8][8 * D + 2];  // L rows, groups in different banks
+    for (int e = threadIdx.x; e < 64; e += blockDim.x) {
+        sW[(e & 7) * 8 + (e >> 3)] = (&c_mu[0][0])[e];
+        sW[72 + (e & 7) * 8 + (e >> 3)] = (&c_nu[0][0])[e];
+    }
+    if (threadIdx.x < 8) {
+        sHB[threadIdx.x] = a.hb[threadIdx.x];
+        sC[threadIdx.x] = c_c[threadIdx.x];
+    }
+    __syncthreads();
+    const double *Mu = sW + s, *Nu = sW + 72 + s;
+    double *G = sG[gib];
+
+    double y[D];
+#pragma unroll
+    for (int l = 0; l < D; ++l) y[l] = a.y[l * B + bb];
+    int64_t bad = a.stats[1 * B + bb];
+    const int64_t n0 = *a.n_done;
+    const bool sample = (a.energy != nullptr) && (a.energy_every > 0);
+    double hprev = 0.0, dhmax = 0.0;
+    if (valid && s == 0) {
+        if (sample && a.c0 == 0) a.energy[b] = prob.energy(y, y + d);
+        if (a.local_energy) hprev = prob.energy(y, y + d);
+    }
+    bool live = valid && bad == 0 && a.nsteps > 0;
+    if (valid && !live && s == 0) {
+        if (a.iters && a.c0 == 0) a.iters[b] = 0;
+        if (a.csweeps) a.csweeps[b] = 0;
+        if (a.local_energy && a.c0 == 0) a.stats[3 * B + b] = 0;
+    }
+    // Y_s^[0] = y + D(nu_s., L_{n-1}) over all D components (history row s -> tile)
+    double Ys[D];
+#pragma unroll
+    for (int l = 0; l < D; ++l) G[s * D + l] = live ? a.hist[((int64_t)s * D + l) * B + b] : 0.0;
+    __syncwarp();
+#pragma unroll
+    for (int l = 0; l < D; ++l) {
+        double acc = dmul(Nu[0], G[l]);
+#pragma unroll
+        for (int j = 1; j < 8; ++j) acc = dfma(Nu[8 * j], G[j * D + l], acc);
+        Ys[l] = dadd(y[l], acc);
+    }
+    __syncwarp();
+    constexpr int64_t kInf = 0x7ff0000000000000LL;
+    int64_t m[D], p[D];
+#pragma unroll
+    for (int l = 0; l < D; ++l) m[l] = p[l] = kInf;
+    int64_t n = 0, hits = 0, sweeps = 0;
+    int k = 0;
+    while (__any_sync(FULL, live)) {  // warp-uniform: the group tiles and votes need every lane
+        ++k;
+        // F_s = f(Y_s, t_s) ; L_s = hb_s F_s -> tile row s
+        const double tn1 = dadd(a.t0, dmul((double)(n0 + n), a.h));
+        const double ts = dadd(tn1, dmul(sC[s], a.h));
+        double Ls[D];
+        {
+            bool ok = true;
+            fo_rhs<P, false>(prob, Ys, Ls, ts, ok);
+            if (!ok) fo_rhs<P, true>(prob, Ys, Ls, ts, ok);  // exact intrinsics, same bits
+        }
+#pragma unroll
+        for (int l = 0; l < D; ++l) G[s * D + l] = Ls[l] = dmul(sHB[s], Ls[l]);
+        __syncwarp();
+        // Yn_s = y + D(mu_s., L) ; Delta over the group ; stop test (from k = 1)
+        bool stop = true;
+        double Yn[D];
+#pragma unroll
+        for (int l = 0; l < D; ++l) {
+            double acc = dmul(Mu[0], G[l]);
+#pragma unroll
+            for (int j = 1; j < 8; ++j) acc = dfma(Mu[8 * j], G[j * D + l], acc);
+            Yn[l] = dadd(y[l], acc);
+            int64_t e = __double_as_longlong(dsub(Yn[l], Ys[l])) & 0x7fffffffffffffffLL;
+            e = (e > kInf) ? 0 : e;  // NaN-ignoring max
+#pragma unroll
+            for (int off = 1; off < 8; off <<= 1) {
+                const int64_t o = __shfl_xor_sync(FULL, e, off);
+                e = (o > e) ? o : e;
+            }
+            const bool okc = (e == 0) || (m[l] <= ((e < p[l]) ? e : p[l]));
+            m[l] = (p[l] < m[l]) ? p[l] : m[l];
+            p[l] = e;
+            stop = stop && okc;
+        }
+        const bool fin = live && (stop || k >= a.max_iters);
+        if (fin) {  // update with this sweep's L (replicated), samples, history row s
+            bool finite = true;
+#pragma unroll
+            for (int l = 0; l < D; ++l) {
+                double sl = G[l];
+#pragma unroll
+                for (int j = 1; j < 8; ++j) sl = dadd(sl, G[j * D + l]);
+                y[l] = dadd(y[l], sl);
+                finite = finite && isfinite(y[l]);
+            }
+            ++n;
+            sweeps += k;
+            hits += stop ? 0 : 1;
+            k = 0;
+#pragma unroll
+            for (int l = 0; l < D; ++l) m[l] = p[l] = kInf;
+            if (s == 0) {
+                if (sample && ((a.c0 + n) % a.energy_every) == 0)
+                    a.energy[((a.c0 + n) / a.energy_every) * B + b] = prob.energy(y, y + d);
+                if (a.local_energy) dhloc_update(prob.energy(y, y + d), hprev, dhmax);
+            }
+            if (n == a.nsteps || !finite) {
+#pragma unroll
+                for (int l = 0; l < D; ++l) a.hist[((int64_t)s * D + l) * B + b] = Ls[l];
+                if (!finite) bad = n0 + n;
+                live = false;
+            }
+            // next step's init: Y_s = y + D(nu_s., L)
+#pragma unroll
+            for (int l = 0; l < D; ++l) {
+                double acc = dmul(Nu[0], G[l]);
+#pragma unroll
+                for (int j = 1; j < 8; ++j) acc = dfma(Nu[8 * j], G[j * D + l], acc);
+                Yn[l] = dadd(y[l], acc);
+            }
+        }
+#pragma unroll
+        for (int l = 0; l < D; ++l) Ys[l] = Yn[l];
+        __syncwarp();  // tile reads done before the next sweep's writes
+    }
+    if (valid && s == 0) {
+#pragma unroll
+        for (int l = 0; l < D; ++l) a.y[l * B + b] = y[l];
+        if (a.nsteps > 0 && a.stats[1 * B + b] == 0) {
+            a.stats[0 * B + b] += hits;
+            a.stats[1 * B + b] = bad;
+            a.stats[2 * B + b] += sweeps;
+            if (a.iters) a.iters[b] = (a.c0 == 0) ? sweeps : a.iters[b] + sweeps;
+            if (a.csweeps) a.csweeps[b] = (int32_t)sweeps;
+            if (a.local_energy) dhloc_store(&a.stats[3 * B + b], a.c0 == 0, dhmax);
+        }
+    }
+}
+
+}  // namespace irk

@@ -65,7 +65,9 @@ namespace {
 
 constexpr size_t kHeader = 64;
 constexpr int64_t kG8AutoMaxBatch = 12288;  // IRK_OPT_MAPPING auto: g8 up to this batch (Kepler, HH)
-constexpr int64_t kN8AutoMaxBatch = 6144;  // IRK_OPT_MAPPING auto: stage-per-lane N-body up to this batch
+constexpr int64_t kN8AutoMaxBatch = 6144;       // IRK_OPT_MAPPING auto: stage-per-lane N-body up to this batch
+constexpr int64_t kFo8AutoMaxBatch = INT64_MAX;  // first-order mode: stage per lane at every measured batch
+                                                 // (tools/fo_bench.py: 1 to 65,536 trajectories)
 
 int fail(irk_ctx *c, int code, const char *fmt, ...) {
     char buf[512];
@@ -503,6 +505,19 @@ template <class P>
 int launch_first_order(irk_ctx *c, const P &prob, double *y, double t0, char *ws, double *energy, int64_t *iters,
                        cudaStream_t st) {
     EnsArgs a = ens_args(c, y, t0, ws, energy, iters);
+    if (c->mapping == IRK_MAP_G8 || (c->mapping == IRK_MAP_AUTO && c->batch <= kFo8AutoMaxBatch)) {
+        a.nsteps = c->nsteps;  // stage per lane: one launch, one group of 8 lanes per trajectory
+        a.c0 = 0;
+        a.csweeps = nullptr;
+        a.perm = nullptr;
+        a.nslots = c->batch;
+        const int64_t blocks = (c->batch * 8 + irk::FO8_THREADS - 1) / irk::FO8_THREADS;
+        irk::ens_fo8_kernel<P><<<(unsigned)blocks, irk::FO8_THREADS, 0, st>>>(a, prob);
+        int rc = cuda_check(c, cudaGetLastError(), "ens_fo8 launch");
+        if (rc) return rc;
+        advance_n_kernel<<<1, 1, 0, st>>>(reinterpret_cast<int64_t *>(ws), c->nsteps);
+        return cuda_check(c, cudaGetLastError(), "advance_n launch");
+    }
     if (c->schedule != 1)
         return launch_queue(c, irk::ens_fo_q_kernel<P>, irk::FO_THREADS, irk::FO_THREADS, &c->fo_blocks_per_sm, a, ws, st,
                             [&](const EnsArgs &aa, const irk::QueueArgs &qa, unsigned nb) {
@@ -798,7 +813,8 @@ int irk_set_option(irk_ctx *c, int key, int64_t val) {
     case IRK_OPT_MAPPING:
         if (val != IRK_MAP_AUTO && val != IRK_MAP_G1 && val != IRK_MAP_G8)
             return fail(c, IRK_E_ARG, "irk_set_option: MAPPING must be 0 (auto), 1 (g1) or 8 (g8)");
-        if (val == IRK_MAP_G8 && c->problem != IRK_KEPLER && c->problem != IRK_HENON_HEILES && c->problem != IRK_NBODY)
+        if (val == IRK_MAP_G8 && c->problem != IRK_KEPLER && c->problem != IRK_HENON_HEILES && c->problem != IRK_NBODY &&
+            c->problem != IRK_SCHWARZSCHILD)
             return fail(c, IRK_E_ARG, "irk_set_option: the g8 mapping is built for Kepler, Henon-Heiles, N-body");
         c->mapping = (int)val;
         return IRK_OK;
