@@ -429,6 +429,26 @@ def test_nbody_stage_per_lane_mapping(irk, orc):
     assert np.array_equal(outs[0][4][idx], o2["dhloc"])
 
 
+def test_million_trajectory_batch(irk, orc):
+    """2^20 Kepler trajectories (18 units of work per queue lane, 16 M-entry
+    SoA rows), 60 steps with energy samples: sampled members bitwise equal to
+    the oracle."""
+    B, ns = 1 << 20, 60
+    w = wl.kepler_ensemble(batch=B, nsteps=ns)
+    with irk.Integrator(w.problem, w.dim, w.h, w.nsteps, w.batch, w.params, energy_every=20) as ig:
+        Y = torch.tensor(w.y, dtype=torch.float64, device="cuda")
+        ws = ig.new_workspace()
+        E = torch.zeros((ig.n_energy(), B), dtype=torch.float64, device="cuda")
+        it = torch.zeros(B, dtype=torch.int64, device="cuda")
+        ig.integrate(Y, ws, energy=E, iters=it)
+        rc, st = ig.stats(ws)
+        idx = np.r_[0, np.arange(1, B, B // 61), B - 1]
+        yg, Eg, itg = Y.cpu().numpy()[:, idx], E.cpu().numpy()[:, idx], it.cpu().numpy()[idx]
+    o = orc.integrate(w.problem, np.ascontiguousarray(w.y[:, idx]), w.params, w.h, w.nsteps, energy_every=20)
+    assert rc == irk.OK
+    assert np.array_equal(yg, o["y"]) and np.array_equal(Eg, o["energy"]) and np.array_equal(itg, o["iters"])
+
+
 # ------------------------------------------------------------------ config 3
 def test_config3_six_body_ragged_energy(irk, orc):
     """Config-3 generator, ragged batch of 37 members, 3,000 steps, energy every
