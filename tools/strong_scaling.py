@@ -1,0 +1,47 @@
+"""Strong scaling of the ensemble configs from single-GPU shard measurements.
+
+The ensembles shard by trajectory with no communication, so the
+time of P GPUs on a batch B is the time of one GPU on its shard B/P (max over
+shards; shards are statistically alike).  For P = 1, 2, 4, 8 we time the first
+B/P trajectories of each config on one B200 with the default (auto) mapping and
+report the projected strong-scaling efficiency T(B) / (P T(B/P)); the bench
+itself reports weak scaling (B per GPU)."""
+import json
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch  # noqa: E402
+
+from paper_2511_03655_b200 import irk, workloads as wl  # noqa: E402
+
+
+def time_call(w, y):
+    B = y.shape[1]
+    with irk.Integrator(w.problem, w.dim, w.h, w.nsteps, B, w.params) as ig:
+        y0 = torch.tensor(y, dtype=torch.float64, device="cuda")
+        Y = torch.empty_like(y0)
+        ws = ig.new_workspace()
+        ts = []
+        for _ in range(3):
+            Y.copy_(y0); ws.zero_(); torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(); ig.integrate(Y, ws); e1.record(); torch.cuda.synchronize()
+            ts.append(e0.elapsed_time(e1))
+        return min(ts[1:])
+
+
+res = []
+for cfg, nsteps in ((2, 10000), (3, 10000), (4, 20000)):
+    w = wl.config(cfg, nsteps=nsteps)
+    t1 = None
+    for P in (1, 2, 4, 8):
+        B = w.batch // P
+        t = time_call(w, w.y[:, :B].copy())
+        t1 = t if P == 1 else t1
+        r = {"config": cfg, "nsteps": nsteps, "P": P, "batch_per_gpu": B, "ms": t,
+             "efficiency": t1 / (P * t), "traj_steps_per_s_total": w.batch * nsteps / (t * 1e-3)}
+        print(json.dumps(r), flush=True)
+        res.append(r)
+if len(sys.argv) > 1:
+    json.dump(res, open(sys.argv[1], "w"), indent=1)
