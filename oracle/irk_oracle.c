@@ -257,10 +257,14 @@ static void accel_kepler(const double *P, const double *q, double *a) {
 }
 
 /* Henon-Heiles, Listing 2 literally:
- *   aux = lambda + xi*sin(t); a1 = -q1 - 2*aux*q1*q2; a2 = -q2 - aux*(q1^2 - q2^2) */
+ *   aux = lambda + xi*sin(t) (canonical sin); a1 = -q1 - 2*aux*q1*q2; a2 = -q2 - aux*(q1^2 - q2^2) */
 static void accel_hh(const double *P, double t, const double *q, double *a) {
     double aux = P[0];
-    if (P[1] != 0.0) aux = P[0] + P[1] * sin(t);
+    if (P[1] != 0.0) {  /* canonical sin (CANON.md, R-12): bitwise the GPU's */
+        double sn, cs;
+        orc_sincos(t, &sn, &cs);
+        aux = P[0] + P[1] * sn;
+    }
     a[0] = -q[0] - ((2.0 * aux) * q[0]) * q[1];
     a[1] = -q[1] - aux * (q[0] * q[0] - q[1] * q[1]);
 }

@@ -30,31 +30,6 @@ struct Kepler {
     }
 };
 
-// Henon-Heiles with the time-dependent coupling of Listing 2 (P:L366-378):
-// aux = lambda + xi sin(t); a1 = -q1 - 2 aux q1 q2; a2 = -q2 - aux (q1^2 - q2^2).
-struct HenonHeiles {
-    static constexpr int d = 2;
-    static constexpr bool first_order = false;
-    double lambda, xi;
-    template <bool EXACT>
-    __device__ __forceinline__ void accel(const double *q, double *a, double t, bool & /*ok*/) const {
-        double aux = lambda;
-        if (xi != 0.0) aux = dadd(lambda, dmul(xi, sin(t)));  // not bitwise vs libm
-        a[0] = dsub(-q[0], dmul(dmul(dmul(2.0, aux), q[0]), q[1]));
-        a[1] = dsub(-q[1], dmul(aux, dsub(dmul(q[0], q[0]), dmul(q[1], q[1]))));
-    }
-    __device__ __forceinline__ double energy(const double *q, const double *v) const {
-        Neumaier n;
-        n.add(dmul(0.5, dmul(v[0], v[0])));
-        n.add(dmul(0.5, dmul(v[1], v[1])));
-        n.add(dmul(0.5, dmul(q[0], q[0])));
-        n.add(dmul(0.5, dmul(q[1], q[1])));
-        n.add(dmul(lambda, dmul(dmul(q[0], q[0]), q[1])));
-        n.add(-dmul(lambda, ddiv(dmul(dmul(q[1], q[1]), q[1]), 3.0)));
-        return n.result();
-    }
-};
-
 // Canonical sine and cosine (oracle/CANON.md "Canonical sin / cos"): x = k pi/2 + t
 // by a three-part Cody-Waite reduction, Taylor polynomials of degree 19 / 20 in
 // t on |t| <= pi/4 (Horner in t^2 with fma), quadrant by k mod 4.  All
@@ -95,6 +70,35 @@ __device__ __forceinline__ void canon_sincos(double x, double &sn, double &cs) {
     default: sn = -ct; cs = st; break;
     }
 }
+
+// Henon-Heiles with the time-dependent coupling of Listing 2 (P:L366-378):
+// aux = lambda + xi sin(t); a1 = -q1 - 2 aux q1 q2; a2 = -q2 - aux (q1^2 - q2^2).
+struct HenonHeiles {
+    static constexpr int d = 2;
+    static constexpr bool first_order = false;
+    double lambda, xi;
+    template <bool EXACT>
+    __device__ __forceinline__ void accel(const double *q, double *a, double t, bool & /*ok*/) const {
+        double aux = lambda;
+        if (xi != 0.0) {  // canonical sin (R-12): bitwise the oracle's
+            double sn, cs;
+            canon_sincos(t, sn, cs);
+            aux = dadd(lambda, dmul(xi, sn));
+        }
+        a[0] = dsub(-q[0], dmul(dmul(dmul(2.0, aux), q[0]), q[1]));
+        a[1] = dsub(-q[1], dmul(aux, dsub(dmul(q[0], q[0]), dmul(q[1], q[1]))));
+    }
+    __device__ __forceinline__ double energy(const double *q, const double *v) const {
+        Neumaier n;
+        n.add(dmul(0.5, dmul(v[0], v[0])));
+        n.add(dmul(0.5, dmul(v[1], v[1])));
+        n.add(dmul(0.5, dmul(q[0], q[0])));
+        n.add(dmul(0.5, dmul(q[1], q[1])));
+        n.add(dmul(lambda, dmul(dmul(q[0], q[0]), q[1])));
+        n.add(-dmul(lambda, ddiv(dmul(dmul(q[1], q[1]), q[1]), 3.0)));
+        return n.result();
+    }
+};
 
 // Charged particle near a magnetised Schwarzschild black hole, Eq. Ham_SBH
 // (P:L508-518), y = (r, theta | p_r, p_theta), parameters {E, L, beta}.

@@ -120,14 +120,23 @@ def test_henon_heiles_parity(irk, orc):
     assert_parity(g, o, energy=True)
 
 
-def test_henon_heiles_time_dependent_close(irk, orc):
-    """xi != 0 uses sin(t): CUDA's sin and libm's differ in the last ulp, so this
-    case is compared at the north-star tolerance only (R-7)."""
-    w = wl.henon_heiles(batch=64, nsteps=500, xi=0.1, lam=1.0)
-    g = run_gpu(irk, w, t0=0.25)
-    o = orc.integrate(w.problem, w.y, w.params, w.h, w.nsteps, t0=0.25)
-    rel = (np.abs(g["y"] - o["y"]).max(axis=0) / np.abs(o["y"]).max(axis=0)).max()
-    assert rel <= 1e-10
+@pytest.mark.parametrize("mode", [0, 1])
+def test_henon_heiles_time_dependent_bitwise(irk, orc, mode):
+    """xi != 0 (Listing 2's time-dependent coupling) uses the canonical sin of
+    CANON.md on both sides (R-12), so the time-dependent case is
+    bitwise too -- partitioned and first-order mode, t0 != 0, chained calls
+    (absolute step index in t_{n-1})."""
+    w = wl.henon_heiles(batch=64, nsteps=500, xi=0.1, lam=1.0, h=0.05 if mode else 2 * math.pi / 68)
+    with irk.Integrator(w.problem, w.dim, w.h, w.nsteps // 2, w.batch, w.params, mode=mode) as ig:
+        Y = torch.tensor(w.y, dtype=torch.float64, device="cuda")
+        ws = ig.new_workspace()
+        it = torch.zeros(w.batch, dtype=torch.int64, device="cuda")
+        ig.integrate(Y, ws, t0=0.25, iters=it)
+        it1 = it.cpu().numpy().copy()
+        ig.integrate(Y, ws, t0=0.25, iters=it)
+        yg, itg = Y.cpu().numpy(), it1 + it.cpu().numpy()
+    o = orc.integrate(w.problem, w.y, w.params, w.h, w.nsteps, t0=0.25, mode=mode)
+    assert np.array_equal(yg, o["y"]) and np.array_equal(itg, o["iters"])
 
 
 def test_max_iters_cap_flagged_like_oracle(irk, orc):
