@@ -477,8 +477,8 @@ def test_config3_full_length_subset(irk, orc):
 
 
 def test_config3_full_batch_sampled(irk, orc):
-    """Config 3 at full batch (16,384 members) in the bench's launch
-    configuration (cost-balanced chunks), 2,000 steps; oracle on 40 sampled members."""
+    """Config 3 at full batch (16,384 members) in the default launch (body-per-lane
+    work queue), 2,000 steps; oracle on 40 sampled members."""
     w = wl.six_body_ensemble(nsteps=2000)
     g = run_gpu(irk, w)
     idx = np.linspace(0, w.batch - 1, 40).astype(int)
@@ -528,8 +528,8 @@ def test_config4_full_length_subset(irk, orc):
 
 
 def test_config4_full_batch_sampled(irk, orc):
-    """Config 4 at full batch (4,096 chains), 3,000 steps, cost-balanced chunks;
-    oracle on 24 sampled chains."""
+    """Config 4 at full batch (4,096 chains), 3,000 steps, default launch (warp-level
+    work queue); oracle on 24 sampled chains."""
     w = wl.fpu_ensemble(nsteps=3000)
     g = run_gpu(irk, w)
     idx = np.linspace(0, w.batch - 1, 24).astype(int)
