@@ -130,9 +130,18 @@ def cpu_baseline(w, target_s: float = 15.0):
     t = time.perf_counter()
     oracle.integrate(w.problem, np.ascontiguousarray(w.y[:, :S]), w.params, w.h, w.nsteps, nthreads=cores)
     dt = time.perf_counter() - t
+    cpu_model = ""
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                cpu_model = line.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
     return {"value": S * w.nsteps / dt, "unit": UNIT, "cores": cores, "kind": "oracle",
+            "value_1core": rate1, "cpu_model": cpu_model,
             "sample": f"first {S} of {w.batch} config-2 trajectories x {w.nsteps} steps "
-                      f"({dt:.1f} s, OpenMP over trajectories)"}
+                      f"({dt:.1f} s, OpenMP over trajectories; value_1core from 8 x 1,000 steps on one core)"}
 
 
 def run_reference(args):
