@@ -85,6 +85,15 @@ enum irk_option {
     IRK_OPT_DEVICE_LOOP = 9,  /* IRK_NBODY_DIRECT: 1 (default) = the fixed-point sweeps run as a CUDA-graph
                                  conditional WHILE loop on the device (one host sync per energy
                                  sample / call); 0 = host loop, one sync per sweep               */
+    IRK_OPT_EXCHANGE = 10,    /* IRK_NBODY_DIRECT under irk_set_comm: how the stage positions reach the
+                                 other ranks each fixed-point iteration.  0 (default) = in-place
+                                 ncclAllGather after the position kernel; 1 = fused: the position
+                                 kernel stores every Q value straight into each rank's copy of its
+                                 slot (a symmetric NCCL window, NVLink load/store, NCCL >= 2.27, all
+                                 ranks in one NVLink domain) and its last CTA signals arrival; the
+                                 next kernel waits for all ranks (IRK_E_COMM after 60 s).  The window
+                                 is created collectively on the first fused irk_integrate and freed
+                                 by irk_destroy.  Bitwise-neutral            */
     IRK_OPT_LOCAL_ENERGY = 7  /* 1: track Delta H^loc_max = max_n |(H(y_n)-H(y_{n-1}))/H(y_{n-1})|
                                  (Eq. DHlocmax) over each call, in-kernel; read it with
                                  irk_local_energy_error (ensemble problems only)                   */

@@ -59,6 +59,11 @@ struct irk_ctx {
     int device_loop = 1;           // IRK_OPT_DEVICE_LOOP (large-N path)
     int device_loop_used = 0;      // IRK_INFO_DEVICE_LOOP_USED: the last call ran the graph loop
     void *nccl_comm = nullptr;
+    // fused exchange (IRK_OPT_EXCHANGE = 1): symmetric NCCL window [header | 2 x P x stride]
+    int exchange = 0;
+    void *xbuf = nullptr, *xwin = nullptr;
+    size_t xbytes = 0, xqoff = 0;
+    void **d_xpeers = nullptr;  // [2P]: rank r's Q buffers, rank r's header (NVLink mapping)
 };
 
 namespace {
@@ -225,6 +230,7 @@ size_t nbd_bytes(const irk_ctx *c) {
 
 int nccl_check(irk_ctx *c, int r, const char *what);
 int nccl_allgather_inplace(irk_ctx *c, double *buf, size_t count_per_rank, cudaStream_t st);
+int xsetup(irk_ctx *c, size_t qbytes, double *scratch, cudaStream_t st);
 
 int launch_direct(irk_ctx *c, double *y, double t0, char *ws, double *energy, int64_t *iters, cudaStream_t st) {
     (void)t0;
@@ -233,7 +239,10 @@ int launch_direct(irk_ctx *c, double *y, double t0, char *ws, double *energy, in
     const int first = c->nccl_comm ? c->rank : 0;
     const int64_t nloc = N / P, dl = 3 * nloc, stride = nbd_stride(c);
     const bool nccl = c->nccl_comm != nullptr;
+    const bool fused = nccl && c->exchange == 1;
     int rc;
+    if (c->exchange == 1 && !nccl)
+        return fail(c, IRK_E_STATE, "irk_integrate: IRK_OPT_EXCHANGE = 1 needs a communicator (irk_set_comm)");
     if (!c->d_mass) {
         if ((rc = cuda_check(c, cudaMalloc(&c->d_mass, sizeof(double) * N), "cudaMalloc mass"))) return rc;
         if ((rc = cuda_check(c, cudaMallocHost(&c->h_ctl, sizeof(irk::NbdCtl)), "cudaMallocHost ctl"))) return rc;
@@ -281,6 +290,22 @@ int launch_direct(irk_ctx *c, double *y, double t0, char *ws, double *energy, in
         a.G = c->params[0];
         a.eps2 = c->params[1] * c->params[1];
         a.max_iters = c->max_iters;
+        a.xmode = 0;
+        a.rank = c->rank;
+        a.peerQ = nullptr;
+        a.peerHdr = nullptr;
+        a.xhdr = nullptr;
+        a.qbuf = (int64_t)P * stride;
+    }
+    if (fused) {
+        // the symmetric window is created on the first fused call (collective: every
+        // rank integrates); one scratch double of `terms` serves the set-up barrier
+        if (!c->xwin && (rc = xsetup(c, sizeof(double) * 2 * (size_t)P * stride, terms, st))) return rc;
+        A[0].xmode = 1;
+        A[0].Qg = reinterpret_cast<double *>(static_cast<char *>(c->xbuf) + c->xqoff);
+        A[0].peerQ = reinterpret_cast<double *const *>(c->d_xpeers);
+        A[0].peerHdr = reinterpret_cast<int64_t *const *>(c->d_xpeers + P);
+        A[0].xhdr = static_cast<int64_t *>(c->xbuf);
     }
     const unsigned cb = (unsigned)((dl + 127) / 128);
     const int64_t E = c->energy_every;
@@ -316,7 +341,7 @@ int launch_direct(irk_ctx *c, double *y, double t0, char *ws, double *energy, in
     // one fixed-point sweep of every local shard (a2+a5, exchange, a3, a4+a6, counters)
     auto enqueue_sweep = [&](cudaStream_t s, cudaGraphConditionalHandle cond, int use_cond) -> int {
         for (int t = 0; t < nlocal; ++t) irk::nbd_pos_kernel<<<cb, 128, 0, s>>>(A[t]);
-        if (nccl) {
+        if (nccl && !fused) {
             int r = nccl_allgather_inplace(c, Qg, (size_t)stride, s);  // the exchange
             if (r) return r;
         }
@@ -401,9 +426,18 @@ int launch_direct(irk_ctx *c, double *y, double t0, char *ws, double *energy, in
             }
         }
     }
+    if (fused && c->h_ctl->xerr) return fail(c, IRK_E_COMM, "fused exchange: a peer did not arrive within 60 s");
     // final exchange: a divergence at the call's last step is recorded on every rank
-    if (nccl && (rc = nccl_allgather_inplace(c, Qg, (size_t)stride, st))) return rc;
-    irk::nbd_final_kernel<<<1, 1, 0, st>>>(A[0], n_done, stats);
+    if (fused) {
+        irk::nbd_xfinal_kernel<<<1, 1, 0, st>>>(A[0], n_done, stats);
+        cudaMemcpyAsync(c->h_ctl, ctl, sizeof(irk::NbdCtl), cudaMemcpyDeviceToHost, st);
+        if ((rc = cuda_check(c, cudaStreamSynchronize(st), "fused exchange final barrier"))) return rc;
+        if (c->h_ctl->xerr)
+            return fail(c, IRK_E_COMM, "fused exchange: a peer did not arrive within %d s", 60);
+    } else {
+        if (nccl && (rc = nccl_allgather_inplace(c, Qg, (size_t)stride, st))) return rc;
+        irk::nbd_final_kernel<<<1, 1, 0, st>>>(A[0], n_done, stats);
+    }
     if (iters) cudaMemcpyAsync(iters, &ctl->sweeps, sizeof(int64_t), cudaMemcpyDeviceToDevice, st);
     return cuda_check(c, cudaGetLastError(), "direct launch");
 }
@@ -655,6 +689,7 @@ __global__ void energy_g1_kernel(const double *y, double *H, int64_t B, const __
 // ---- NCCL (loaded at run time: the library has no link-time NCCL dependency) ----
 #include <dlfcn.h>
 #include "nccl.h"
+#include "nccl_device.h"  // ncclGetPeerPointer (device-inline window mapping) for the fused exchange
 
 namespace {
 struct NcclApi {
@@ -664,6 +699,12 @@ struct NcclApi {
     ncclResult_t (*allGather)(const void *, void *, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
     ncclResult_t (*commDestroy)(ncclComm_t) = nullptr;
     const char *(*getErrorString)(ncclResult_t) = nullptr;
+    // symmetric windows (fused exchange); absent in older NCCL: the option then fails
+    ncclResult_t (*memAlloc)(void **, size_t) = nullptr;
+    ncclResult_t (*memFree)(void *) = nullptr;
+    ncclResult_t (*winRegister)(ncclComm_t, void *, size_t, ncclWindow_t *, int) = nullptr;
+    ncclResult_t (*winDeregister)(ncclComm_t, ncclWindow_t) = nullptr;
+    ncclTeam_t (*teamLsa)(ncclComm_t) = nullptr;
 };
 std::mutex g_nccl_mu;
 NcclApi g_nccl;
@@ -683,6 +724,11 @@ const char *load_nccl() {
     g_nccl.allGather = (decltype(g_nccl.allGather))dlsym(h, "ncclAllGather");
     g_nccl.commDestroy = (decltype(g_nccl.commDestroy))dlsym(h, "ncclCommDestroy");
     g_nccl.getErrorString = (decltype(g_nccl.getErrorString))dlsym(h, "ncclGetErrorString");
+    g_nccl.memAlloc = (decltype(g_nccl.memAlloc))dlsym(h, "ncclMemAlloc");
+    g_nccl.memFree = (decltype(g_nccl.memFree))dlsym(h, "ncclMemFree");
+    g_nccl.winRegister = (decltype(g_nccl.winRegister))dlsym(h, "ncclCommWindowRegister");
+    g_nccl.winDeregister = (decltype(g_nccl.winDeregister))dlsym(h, "ncclCommWindowDeregister");
+    g_nccl.teamLsa = (decltype(g_nccl.teamLsa))dlsym(h, "ncclTeamLsa");
     if (!g_nccl.getUniqueId || !g_nccl.commInitRank || !g_nccl.allGather || !g_nccl.commDestroy)
         return "NCCL library lacks required symbols";
     g_nccl.h = h;
@@ -699,6 +745,56 @@ int nccl_allgather_inplace(irk_ctx *c, double *buf, size_t count_per_rank, cudaS
     return nccl_check(c, g_nccl.allGather(buf + (size_t)c->rank * count_per_rank, buf, count_per_rank, ncclFloat64,
                                           comm, st),
                       "ncclAllGather");
+}
+
+// rank r's view of the window through the NVLink (LSA) mapping: its Q buffers and header
+__global__ void xpeers_kernel(ncclWindow_t w, int P, size_t qoff, void **out) {
+    const int r = threadIdx.x;
+    if (r >= P) return;
+    out[r] = ncclGetPeerPointer(w, qoff, r);
+    out[P + r] = ncclGetPeerPointer(w, 0, r);
+}
+
+// Fused exchange set-up (collective over the communicator; NEXT f3): one symmetric
+// window [header | Q buffer 0 | Q buffer 1] per rank from ncclMemAlloc, registered
+// with NCCL_WIN_COLL_SYMMETRIC so that every rank reaches every other rank's copy
+// through NVLink load/store; zero-filled, then a 1-double all-gather as a barrier
+// so that no rank pushes into a window before its owner has cleared it.
+int xsetup(irk_ctx *c, size_t qbytes, double *scratch, cudaStream_t st) {
+    ncclComm_t comm = reinterpret_cast<ncclComm_t>(c->nccl_comm);
+    const int P = c->nranks;
+    if (!g_nccl.memAlloc || !g_nccl.memFree || !g_nccl.winRegister || !g_nccl.winDeregister)
+        return fail(c, IRK_E_COMM, "fused exchange: this NCCL has no symmetric windows (needs >= 2.27)");
+    if (g_nccl.teamLsa) {
+        const ncclTeam_t lsa = g_nccl.teamLsa(comm);
+        if (lsa.nRanks != P)
+            return fail(c, IRK_E_COMM, "fused exchange: %d of %d ranks share a load/store (NVLink) domain", lsa.nRanks, P);
+    }
+    const size_t hdr = ((sizeof(int64_t) * (P + irk::kXHeaderExtra)) + 4095) / 4096 * 4096;
+    const size_t bytes = (hdr + qbytes + 4095) / 4096 * 4096;
+    void *buf = nullptr;
+    int rc = nccl_check(c, g_nccl.memAlloc(&buf, bytes), "ncclMemAlloc");
+    if (rc) return rc;
+    if ((rc = cuda_check(c, cudaMemsetAsync(buf, 0, bytes, st), "memset window")) ||
+        (rc = cuda_check(c, cudaStreamSynchronize(st), "memset window"))) {
+        g_nccl.memFree(buf);
+        return rc;
+    }
+    ncclWindow_t win = nullptr;
+    if ((rc = nccl_check(c, g_nccl.winRegister(comm, buf, bytes, &win, NCCL_WIN_COLL_SYMMETRIC),
+                         "ncclCommWindowRegister"))) {
+        g_nccl.memFree(buf);
+        return rc;
+    }
+    c->xbuf = buf;
+    c->xwin = win;
+    c->xbytes = bytes;
+    c->xqoff = hdr;
+    if ((rc = cuda_check(c, cudaMalloc(&c->d_xpeers, sizeof(void *) * 2 * P), "cudaMalloc peers"))) return rc;
+    xpeers_kernel<<<1, (P + 31) / 32 * 32, 0, st>>>(win, P, hdr, c->d_xpeers);
+    if ((rc = cuda_check(c, cudaGetLastError(), "peer pointers"))) return rc;
+    if ((rc = nccl_allgather_inplace(c, scratch, 1, st))) return rc;
+    return cuda_check(c, cudaStreamSynchronize(st), "window set-up barrier");
 }
 }  // namespace
 
@@ -802,6 +898,12 @@ int irk_set_option(irk_ctx *c, int key, int64_t val) {
             return fail(c, IRK_E_ARG, "irk_set_option: VSHARDS needs IRK_NBODY_DIRECT, N %% P == 0, no NCCL comm");
         c->vshards = (int)val;
         return IRK_OK;
+    case IRK_OPT_EXCHANGE:
+        if (c->problem != IRK_NBODY_DIRECT || (val != 0 && val != 1))
+            return fail(c, IRK_E_ARG, "irk_set_option: EXCHANGE is 0 or 1, for IRK_NBODY_DIRECT");
+        if (c->xwin && val != 1) return fail(c, IRK_E_STATE, "irk_set_option: the fused exchange window is in use");
+        c->exchange = (int)val;
+        return IRK_OK;
     case IRK_OPT_DEVICE_LOOP:
         if (val != 0 && val != 1) return fail(c, IRK_E_ARG, "irk_set_option: DEVICE_LOOP must be 0 or 1");
         c->device_loop = (int)val;
@@ -834,6 +936,7 @@ int irk_get_option(const irk_ctx *c, int key, int64_t *val) {
     case IRK_OPT_LOCAL_ENERGY: *val = c->local_energy; return IRK_OK;
     case IRK_OPT_SCHEDULE: *val = c->schedule; return IRK_OK;
     case IRK_OPT_DEVICE_LOOP: *val = c->device_loop; return IRK_OK;
+    case IRK_OPT_EXCHANGE: *val = c->exchange; return IRK_OK;
     case IRK_INFO_DEVICE_LOOP_USED: *val = c->device_loop_used; return IRK_OK;
     }
     return IRK_E_ARG;
@@ -1095,6 +1198,10 @@ void irk_destroy(irk_ctx *c) {
     cudaFree(c->d_ws);
     cudaFree(c->d_mass);
     cudaFree(c->d_rows);
+    cudaFree(c->d_xpeers);
+    if (c->xwin && g_nccl.winDeregister)
+        g_nccl.winDeregister(reinterpret_cast<ncclComm_t>(c->nccl_comm), reinterpret_cast<ncclWindow_t>(c->xwin));
+    if (c->xbuf && g_nccl.memFree) g_nccl.memFree(c->xbuf);
     if (c->nccl_comm && g_nccl.commDestroy) g_nccl.commDestroy(reinterpret_cast<ncclComm_t>(c->nccl_comm));
     if (c->h_ctl) cudaFreeHost(c->h_ctl);
     delete c;

@@ -13,7 +13,13 @@
 //   (exchange)            ncclAllGather in place on Qg (NCCL mode) -- the one
 //                         data-path collective, once per iteration;
 //                         nothing to do for virtual shards (shared buffer).
-//   nbd_or                global stop = no flag set in any slot (same on every rank).
+//                         Fused mode (IRK_OPT_EXCHANGE = 1, NEXT f3): no separate
+//                         collective -- nbd_pos stores each Q^[k] value straight into
+//                         every rank's copy of its slot (NVLink peer pointers of a
+//                         symmetric NCCL window) and its last CTA signals arrival to
+//                         every rank; see "Fused exchange" below.
+//   nbd_or                global stop = no flag set in any slot (same on every rank);
+//                         fused mode: first waits for every rank's arrival.
 //   nbd_force  (a3)       (local body, stage, j-block) parallel: the canonical blocked
 //                         direct sum (R-8) over ALL N bodies read from Qg,
 //                         one thread = one partial sum over NBD_JBLOCK = 1024 bodies j
@@ -43,7 +49,7 @@ struct NbdCtl {           // device-side control block (one per process)
     int32_t fin;          // last sweep finished a step
     int32_t nonfinite;    // global (after an exchange): some component became non-finite
     int32_t halt;         // stop integrating (divergence)
-    int32_t pad;
+    int32_t xerr;         // fused exchange: a peer's arrival timed out (IRK_E_COMM)
     int64_t sweeps, hits;
     int64_t target;       // device-driven loop: run sweeps until n == target (or halt)
 };
@@ -67,15 +73,89 @@ struct NbdArgs {
     int shard, nshards;
     double G, eps2;
     int max_iters;
+    // fused exchange (xmode = 1): Qg is this rank's view of a symmetric NCCL window
+    // holding two buffers [2][P][stride]; the sweep of exchange epoch e uses buffer
+    // e & 1.  peerQ[r] = rank r's Qg and peerHdr[r] = rank r's header, both through
+    // the NVLink (LSA) mapping; xhdr = this rank's header (see kX* below).
+    int xmode, rank;
+    double *const *peerQ;
+    int64_t *const *peerHdr;
+    int64_t *xhdr;
+    int64_t qbuf;         // doubles per buffer (P * stride)
 };
 
-__device__ __forceinline__ double *nbd_slot(const NbdArgs &a, int s) { return a.Qg + (int64_t)s * a.stride; }
+// Fused exchange header (int64 words of the window, before the Q buffers):
+// [0, P) arrival epochs written by the peers (word r: rank r's last arrival),
+// then local words: the epoch (barriers passed), the CTA counter of nbd_pos and
+// the OR of its CTAs' "not converged" votes.
+__device__ __forceinline__ int64_t *nbd_xepoch(const NbdArgs &a) { return a.xhdr + a.nshards; }
+__device__ __forceinline__ int64_t *nbd_xcount(const NbdArgs &a) { return a.xhdr + a.nshards + 1; }
+__device__ __forceinline__ int64_t *nbd_xnotok(const NbdArgs &a) { return a.xhdr + a.nshards + 2; }
+constexpr int kXHeaderExtra = 3;
+
+// gathered-slot buffer of the current sweep (buffer 0 unless fused)
+__device__ __forceinline__ double *nbd_cur(const NbdArgs &a) {
+    return a.xmode ? a.Qg + (*nbd_xepoch(a) & 1) * a.qbuf : a.Qg;
+}
+__device__ __forceinline__ double *nbd_slot(const NbdArgs &a, double *buf, int s) { return buf + (int64_t)s * a.stride; }
+__device__ __forceinline__ double *nbd_slot(const NbdArgs &a, int s) { return nbd_slot(a, nbd_cur(a), s); }
 __device__ __forceinline__ int64_t nbd_flag_index(const NbdArgs &a) { return 24 * a.nloc; }
+// element o of this rank's slot in buffer b of rank r's window (NVLink store target)
+__device__ __forceinline__ double *nbd_peer(const NbdArgs &a, int r, int64_t b, int64_t o) {
+    return a.peerQ[r] + (b & 1) * a.qbuf + (int64_t)a.shard * a.stride + o;
+}
+
+__device__ __forceinline__ int64_t ld_acquire_sys(const int64_t *p) {
+    int64_t v;
+    asm volatile("ld.acquire.sys.global.b64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ uint64_t nbd_globaltimer() {
+    uint64_t t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+constexpr uint64_t kXTimeoutNs = 60ull * 1000000000ull;  // a peer that has not arrived in 60 s: IRK_E_COMM
+
+// Barrier wait of the fused exchange (one thread): every rank's arrival word >= e + 1.
+__device__ __forceinline__ bool nbd_xwait(const NbdArgs &a, int64_t e) {
+    const uint64_t t0 = nbd_globaltimer();
+    for (int r = 0; r < a.nshards; ++r)
+        while (ld_acquire_sys(a.xhdr + r) < e + 1) {
+            if (nbd_globaltimer() - t0 > kXTimeoutNs) return false;
+            __nanosleep(64);
+        }
+    return true;
+}
+// Barrier arrival (one thread): publish e + 1 to every rank (release pattern: a
+// system-scope fence, cumulative over every store that happens before it, then
+// relaxed stores; the waiter's ld.acquire.sys completes the synchronisation).
+__device__ __forceinline__ void nbd_xarrive(const NbdArgs &a, int64_t e) {
+    asm volatile("fence.acq_rel.sys;" ::: "memory");  // one release fence, then relaxed stores
+    for (int r = 0; r < a.nshards; ++r)
+        asm volatile("st.relaxed.sys.global.b64 [%0], %1;" ::"l"(a.peerHdr[r] + a.rank), "l"(e + 1) : "memory");
+}
+// After barrier e: read the flags of buffer e & 1 from every slot, then clear this
+// rank's flags in buffer (e + 1) & 1 of every rank (their last readers, the barrier
+// e - 1 waits, are all behind barrier e; their next writers are this rank's own
+// nbd_vel of this sweep and nbd_pos of the next, both later in stream order).
+__device__ __forceinline__ void nbd_xflags(const NbdArgs &a, int64_t e, int &notok, int &bad) {
+    double *buf = a.Qg + (e & 1) * a.qbuf;
+    notok = bad = 0;
+    for (int s = 0; s < a.nshards; ++s) {
+        notok |= (__ldcv(nbd_slot(a, buf, s) + nbd_flag_index(a)) != 0.0);
+        bad |= (__ldcv(nbd_slot(a, buf, s) + nbd_flag_index(a) + 1) != 0.0);
+    }
+    for (int r = 0; r < a.nshards; ++r) {
+        *nbd_peer(a, r, e + 1, nbd_flag_index(a)) = 0.0;
+        *nbd_peer(a, r, e + 1, nbd_flag_index(a) + 1) = 0.0;
+    }
+}
 
 __global__ void nbd_init_kernel(const __grid_constant__ NbdArgs a) {
     const int64_t dl = 3 * a.nloc;
     const int64_t l = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (l == 0) {
+    if (l == 0 && !a.xmode) {  // fused: cleared by the previous barrier (nbd_xflags)
         nbd_slot(a, a.shard)[nbd_flag_index(a)] = 0.0;
         nbd_slot(a, a.shard)[nbd_flag_index(a) + 1] = 0.0;
     }
@@ -99,41 +179,91 @@ __global__ void nbd_init_kernel(const __grid_constant__ NbdArgs a) {
 __global__ void nbd_pos_kernel(const __grid_constant__ NbdArgs a) {
     const int64_t dl = 3 * a.nloc;
     const int64_t l = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (l >= dl) return;
     const int k = a.ctl->k + 1;
-    double *Q = nbd_slot(a, a.shard);
-    const double q = a.yq[l];
-    double Lq[8];
+    const int64_t e = a.xmode ? *nbd_xepoch(a) : 0;
+    // own slot: Q^[k-1] is read from it; Q^[k] goes to it (NCCL / one GPU) or, fused,
+    // to this rank's slot of buffer e & 1 in every rank's window (Q^[k-1] is in e - 1)
+    double *Q = a.xmode ? nbd_slot(a, a.Qg + ((e + 1) & 1) * a.qbuf, a.shard) : nbd_slot(a, a.shard);
+    bool ok = true;
+    if (l < dl) {
+        const double q = a.yq[l];
+        double Lq[8];
 #pragma unroll
-    for (int j = 0; j < 8; ++j) Lq[j] = dmul(a.hb[j], a.V[(int64_t)j * dl + l]);
-    double s = Lq[0];
+        for (int j = 0; j < 8; ++j) Lq[j] = dmul(a.hb[j], a.V[(int64_t)j * dl + l]);
+        double s = Lq[0];
 #pragma unroll
-    for (int j = 1; j < 8; ++j) s = dadd(s, Lq[j]);
-    a.sLq[l] = s;
-    double delta = 0.0;
+        for (int j = 1; j < 8; ++j) s = dadd(s, Lq[j]);
+        a.sLq[l] = s;
+        double delta = 0.0;
 #pragma unroll
-    for (int i = 0; i < 8; ++i) {
-        double acc = dmul(c_mu[i][0], Lq[0]);
+        for (int i = 0; i < 8; ++i) {
+            double acc = dmul(c_mu[i][0], Lq[0]);
 #pragma unroll
-        for (int j = 1; j < 8; ++j) acc = dfma(c_mu[i][j], Lq[j], acc);
-        const double qn = dadd(q, acc);
-        const double e = dabs(dsub(qn, Q[(int64_t)i * dl + l]));
-        delta = (e > delta) ? e : delta;
-        Q[(int64_t)i * dl + l] = qn;
+            for (int j = 1; j < 8; ++j) acc = dfma(c_mu[i][j], Lq[j], acc);
+            const double qn = dadd(q, acc);
+            const double d = dabs(dsub(qn, Q[(int64_t)i * dl + l]));
+            delta = (d > delta) ? d : delta;
+            if (a.xmode) {
+#ifdef NBD_XSELF_LOCAL
+                a.Qg[(e & 1) * a.qbuf + (int64_t)a.shard * a.stride + (int64_t)i * dl + l] = qn;
+                for (int r = 0; r < a.nshards; ++r)
+                    if (r != a.rank) *nbd_peer(a, r, e, (int64_t)i * dl + l) = qn;
+#else
+                for (int r = 0; r < a.nshards; ++r) *nbd_peer(a, r, e, (int64_t)i * dl + l) = qn;
+#endif
+            } else {
+                Q[(int64_t)i * dl + l] = qn;
+            }
+        }
+        if (k >= 2) {
+            const double pl = a.Pst[l], ml = a.M[l];
+            const double mn = (delta < pl) ? delta : pl;
+            ok = (delta == 0.0) || (ml <= mn);
+            a.M[l] = (pl < ml) ? pl : ml;
+            a.Pst[l] = delta;
+            if (!ok && !a.xmode) Q[nbd_flag_index(a)] = 1.0;  // benign race: every writer stores 1
+        }
     }
-    if (k >= 2) {
-        const double pl = a.Pst[l], ml = a.M[l];
-        const double mn = (delta < pl) ? delta : pl;
-        const bool ok = (delta == 0.0) || (ml <= mn);
-        a.M[l] = (pl < ml) ? pl : ml;
-        a.Pst[l] = delta;
-        if (!ok) Q[nbd_flag_index(a)] = 1.0;  // benign race: every writer stores 1
+    if (!a.xmode) return;
+    // Fused exchange epilogue: the CTA's threads' votes are OR-ed at the CTA barrier
+    // (which also orders their stores before thread 0's); thread 0 takes a ticket
+    // with an acq_rel atomic; the CTA with the last ticket pushes the "not
+    // converged" flag and signals arrival e + 1 to every rank after a system-scope
+    // release fence (cumulative: every CTA's stores happen before the arrival -- the
+    // CTA-barrier-then-release pattern of NCCL's own LSA barrier).
+    const int bad = __syncthreads_or(!ok);
+    if (threadIdx.x == 0) {
+        unsigned long long *cnt = reinterpret_cast<unsigned long long *>(nbd_xcount(a));
+        unsigned long long *nok = reinterpret_cast<unsigned long long *>(nbd_xnotok(a));
+        if (bad) atomicOr(nok, 1ull);
+        // acq_rel at gpu scope: this CTA's stores are released to, and every earlier
+        // CTA's acquired by, the CTA that takes the last ticket
+        unsigned long long prev;
+        asm volatile("atom.acq_rel.gpu.global.add.u64 %0, [%1], 1;" : "=l"(prev) : "l"(cnt) : "memory");
+        if (prev == gridDim.x - 1) {
+            const bool any = atomicExch(nok, 0ull) != 0ull;
+            *cnt = 0ull;
+            if (any)
+                for (int r = 0; r < a.nshards; ++r) *nbd_peer(a, r, e, nbd_flag_index(a)) = 1.0;
+            nbd_xarrive(a, e);
+        }
     }
 }
 
 // global flags from every slot (after the exchange)
 __global__ void nbd_or_kernel(const __grid_constant__ NbdArgs a) {
     int any = 0, bad = 0;
+    if (a.xmode) {  // fused: barrier e (every rank's Q^[k] and flags are in), then the flags
+        const int64_t e = *nbd_xepoch(a);
+        if (!nbd_xwait(a, e)) {
+            a.ctl->xerr = 1;
+            return;
+        }
+        nbd_xflags(a, e, any, bad);
+        a.ctl->notok = any;
+        a.ctl->nonfinite = bad;
+        return;
+    }
     for (int s = 0; s < a.nshards; ++s) {
         any |= (nbd_slot(a, s)[nbd_flag_index(a)] != 0.0);
         bad |= (nbd_slot(a, s)[nbd_flag_index(a) + 1] != 0.0);
@@ -149,15 +279,16 @@ __global__ void __launch_bounds__(NBD_FORCE_THREADS) nbd_force_kernel(const __gr
     const int i = blockIdx.y, J = blockIdx.z;
     const int64_t j0 = (int64_t)J * NBD_JBLOCK;
     const int nj = (int)((N - j0) < NBD_JBLOCK ? (N - j0) : NBD_JBLOCK);
+    double *cur = nbd_cur(a);
     for (int t = threadIdx.x; t < nj; t += blockDim.x) {
         const int64_t j = j0 + t;
-        const double *Qj = nbd_slot(a, (int)(j / nloc)) + (int64_t)i * dl + 3 * (j % nloc);
+        const double *Qj = nbd_slot(a, cur, (int)(j / nloc)) + (int64_t)i * dl + 3 * (j % nloc);
         sj[t] = make_double4(Qj[0], Qj[1], Qj[2], a.mass[j]);
     }
     __syncthreads();
     const int64_t body = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;  // local index
     if (body >= nloc) return;
-    const double *Qa = nbd_slot(a, a.shard) + (int64_t)i * dl + 3 * body;
+    const double *Qa = nbd_slot(a, cur, a.shard) + (int64_t)i * dl + 3 * body;
     const double qx = Qa[0], qy = Qa[1], qz = Qa[2];
     double px = 0.0, py = 0.0, pz = 0.0;
     bool ok = true;
@@ -195,7 +326,7 @@ __global__ void nbd_vel_kernel(const __grid_constant__ NbdArgs a) {
     const int64_t dl = 3 * a.nloc;
     const int64_t l = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (l >= dl) return;
-    if (a.ctl->nonfinite) return;  // diverged at the previous step: frozen (R-10)
+    if (a.ctl->nonfinite || a.ctl->xerr) return;  // diverged at the previous step: frozen (R-10)
     const int nj = (int)((a.nbody + NBD_JBLOCK - 1) / NBD_JBLOCK);
     const int k = a.ctl->k + 1;
     const bool stop = (k >= 2) && (a.ctl->notok == 0);
@@ -216,7 +347,14 @@ __global__ void nbd_vel_kernel(const __grid_constant__ NbdArgs a) {
         v = dadd(v, sv);
         a.yq[l] = q;
         a.yv[l] = v;
-        if (!isfinite(q) || !isfinite(v)) nbd_slot(a, a.shard)[nbd_flag_index(a) + 1] = 1.0;
+        if (!isfinite(q) || !isfinite(v)) {
+            if (a.xmode) {  // into buffer e + 1, read after the next barrier
+                const int64_t e = *nbd_xepoch(a);
+                for (int r = 0; r < a.nshards; ++r) *nbd_peer(a, r, e + 1, nbd_flag_index(a) + 1) = 1.0;
+            } else {
+                nbd_slot(a, a.shard)[nbd_flag_index(a) + 1] = 1.0;
+            }
+        }
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
             a.hist[(int64_t)j * a.hdim + a.hq + l] = 0.0;
@@ -241,9 +379,13 @@ __global__ void nbd_vel_kernel(const __grid_constant__ NbdArgs a) {
 __global__ void nbd_ctl_kernel(const __grid_constant__ NbdArgs a, int first_local, int nlocal, int64_t *n_done,
                                int64_t *stats, cudaGraphConditionalHandle cond, int use_cond) {
     NbdCtl *c = a.ctl;
-    for (int s = first_local; s < first_local + nlocal; ++s) nbd_slot(a, s)[nbd_flag_index(a)] = 0.0;
-    if (c->nonfinite) {  // some shard diverged at the last completed step
-        if (stats[1] == 0) stats[1] = *n_done;
+    if (a.xmode) {
+        *nbd_xepoch(a) += 1;  // barrier e passed: the next sweep uses the other buffer
+    } else {
+        for (int s = first_local; s < first_local + nlocal; ++s) nbd_slot(a, s)[nbd_flag_index(a)] = 0.0;
+    }
+    if (c->nonfinite || c->xerr) {  // some shard diverged at the last completed step (or a peer is gone)
+        if (c->nonfinite && stats[1] == 0) stats[1] = *n_done;
         c->halt = 1;
         c->fin = 0;
         if (use_cond) cudaGraphSetConditional(cond, 0);
@@ -272,6 +414,22 @@ __global__ void nbd_ctl_kernel(const __grid_constant__ NbdArgs a, int first_loca
 __global__ void nbd_final_kernel(const __grid_constant__ NbdArgs a, int64_t *n_done, int64_t *stats) {
     int bad = 0;
     for (int s = 0; s < a.nshards; ++s) bad |= (nbd_slot(a, s)[nbd_flag_index(a) + 1] != 0.0);
+    if (bad && stats[1] == 0) stats[1] = *n_done;
+}
+
+// fused mode, after a call's last sweep: one more barrier (epoch e) so that a
+// divergence at the last step (nbd_vel's flag in buffer e & 1) is seen by every
+// rank, exactly as the NCCL mode's final all-gather
+__global__ void nbd_xfinal_kernel(const __grid_constant__ NbdArgs a, int64_t *n_done, int64_t *stats) {
+    const int64_t e = *nbd_xepoch(a);
+    nbd_xarrive(a, e);
+    if (!nbd_xwait(a, e)) {
+        a.ctl->xerr = 1;
+        return;
+    }
+    int notok, bad;
+    nbd_xflags(a, e, notok, bad);
+    *nbd_xepoch(a) = e + 1;
     if (bad && stats[1] == 0) stats[1] = *n_done;
 }
 

@@ -19,6 +19,8 @@ OPT_LOCAL_ENERGY = 7
 OPT_SCHEDULE = 8
 MAP_AUTO, MAP_G1, MAP_G8 = 0, 1, 8  # IRK_OPT_MAPPING (include/irk.h)
 OPT_DEVICE_LOOP = 9
+OPT_EXCHANGE = 10  # IRK_NBODY_DIRECT under set_comm: 0 = ncclAllGather, 1 = fused NVLink stores
+EXCHANGE_ALLGATHER, EXCHANGE_FUSED = 0, 1
 INFO_DEVICE_LOOP_USED = 100
 PARTITIONED, FIRST_ORDER = 0, 1
 
@@ -98,7 +100,7 @@ class Integrator:
     def __init__(self, problem: int, dim: int, h: float, nsteps: int, batch: int, params,
                  *, mode: int | None = None, max_iters: int = 100, energy_every: int = 0,
                  mapping: int = 0, balance: int = -1, vshards: int = 1, local_energy: bool = False,
-                 schedule: int = 0, device_loop: int = 1):
+                 schedule: int = 0, device_loop: int = 1, exchange: int = 0):
         L = lib()
         self._ctx = L.irk_create(problem, dim, h, nsteps, batch)
         if not self._ctx:
@@ -119,6 +121,7 @@ class Integrator:
             self._check(L.irk_set_option(self._ctx, OPT_LOCAL_ENERGY, 1))
         if problem == NBODY_DIRECT:
             self._check(L.irk_set_option(self._ctx, OPT_DEVICE_LOOP, device_loop))
+            self._check(L.irk_set_option(self._ctx, OPT_EXCHANGE, exchange))
         self.rank, self.nranks = 0, 1
 
     def set_comm(self, unique_id: bytes, rank: int, nranks: int):
@@ -203,6 +206,10 @@ class Integrator:
             self._check(rc)
         return rc, dict(maxiter_traj=int(out[0]), diverged_traj=int(out[1]),
                         first_bad_step=int(out[2]), total_sweeps=int(out[3]))
+
+    def set_option(self, key: int, val: int):
+        """irk_set_option (include/irk.h enum irk_option)."""
+        self._check(lib().irk_set_option(self._ctx, key, val))
 
     def get_option(self, key: int) -> int:
         """irk_get_option: an IRK_OPT_* value or an IRK_INFO_* fact about the last call."""

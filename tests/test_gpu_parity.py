@@ -661,6 +661,61 @@ def test_config5_nccl_single_rank_path(irk, orc):
         assert H[0] == orc.energy(w.problem, w.dim, w.params, o["y"][:, 0])
 
 
+def _direct_comm_run(irk, w, exchange, calls=1, energy_every=0, device_loop=1, y=None):
+    """IRK_NBODY_DIRECT under a 1-rank communicator, `calls` chained calls of w.nsteps."""
+    try:
+        uid = irk.nccl_unique_id()
+    except irk.IrkError:
+        pytest.skip("NCCL not loadable")
+    with irk.Integrator(w.problem, w.dim, w.h, w.nsteps, 1, w.params, energy_every=energy_every,
+                        device_loop=device_loop, exchange=exchange) as ig:
+        ig.set_comm(uid, 0, 1)
+        Y = torch.tensor(w.y if y is None else y, dtype=torch.float64, device="cuda")
+        ws = ig.new_workspace()
+        E = (torch.zeros((ig.n_energy(), 1), dtype=torch.float64, device="cuda") if energy_every else None)
+        it = torch.zeros(1, dtype=torch.int64, device="cuda")
+        Es, its = [], 0
+        for _ in range(calls):
+            ig.integrate(Y, ws, energy=E, iters=it)
+            its += int(it.item())
+            if E is not None:
+                Es.append(E.cpu().numpy().copy())
+        rc, st = ig.stats(ws)
+        assert ig.get_option(irk.OPT_EXCHANGE) == exchange
+        return dict(y=Y.cpu().numpy(), iters=its, rc=rc, stats=st,
+                    energy=(np.concatenate([Es[0]] + [e[1:] for e in Es[1:]]) if Es else None),
+                    loop=ig.get_option(irk.INFO_DEVICE_LOOP_USED))
+
+
+@pytest.mark.parametrize("device_loop", [1, 0])
+def test_config5_fused_exchange_single_rank(irk, orc, device_loop):
+    """IRK_OPT_EXCHANGE = 1 (NEXT f3): nbd_pos stores Q^[k] through the NVLink
+    mapping of a symmetric NCCL window, its last CTA signals arrival, nbd_or waits
+    -- double-buffered by exchange epoch.  One rank (the box has one GPU): the
+    peer-pointer stores, the arrival/wait barrier and the buffer/flag parity over
+    three chained calls (odd sweep counts flip the parity) give the oracle's bits."""
+    w = wl.plummer(N=512, nsteps=5)
+    o = orc.integrate(w.problem, w.y, w.params, w.h, 15, energy_every=5)
+    g = _direct_comm_run(irk, w, 1, calls=3, energy_every=5, device_loop=device_loop)
+    assert g["loop"] == device_loop
+    assert np.array_equal(g["y"], o["y"])
+    assert np.array_equal(g["energy"], o["energy"])
+    assert g["iters"] == int(o["iters"][0]) and g["rc"] == irk.OK
+
+
+def test_config5_fused_exchange_divergence(irk):
+    """A non-finite body: the divergence flag travels through the fused exchange
+    (nbd_vel's store into the next buffer, the final barrier) exactly as through
+    the all-gather -- same frozen state, same first bad step, same sweep count."""
+    w = wl.plummer(N=256, nsteps=6)
+    y = w.y.copy()
+    y[3 * 256 + 7, 0] = np.inf  # a velocity component of body 2
+    outs = [_direct_comm_run(irk, w, ex, calls=2, y=y) for ex in (0, 1)]
+    assert outs[0]["rc"] == irk.E_DIVERGED and outs[1]["rc"] == irk.E_DIVERGED
+    assert outs[0]["stats"] == outs[1]["stats"] and outs[0]["iters"] == outs[1]["iters"]
+    assert np.array_equal(outs[0]["y"], outs[1]["y"], equal_nan=True)
+
+
 # ------------------------------------------------- local energy error (f2)
 @pytest.mark.parametrize("which", ["kepler", "hh", "hh_fo", "nbody", "fpu"])
 def test_local_energy_error_parity(irk, orc, which):

@@ -83,6 +83,13 @@ def test_params_and_options_errors(irk):
     with pytest.raises(irk.IrkError):  # first-order mode is built for the per-thread problems only
         irk.Integrator(irk.FPU_BETA, 128, 0.1, 10, 4, params=[1.0], mode=irk.FIRST_ORDER)
     irk.Integrator(irk.HENON_HEILES, 4, 0.1, 10, 4, params=[1.0, 0.0], mode=irk.FIRST_ORDER).close()
+    with pytest.raises(irk.IrkError):  # the fused exchange is an IRK_NBODY_DIRECT option
+        irk.Integrator(irk.KEPLER, 4, 0.1, 10, 4, params=[1.0]).set_option(irk.OPT_EXCHANGE, 1)
+    with pytest.raises(irk.IrkError):
+        irk.Integrator(irk.NBODY_DIRECT, 6 * 64, 0.1, 10, 1, params=[1.0, 0.01] + [1 / 64] * 64, exchange=2)
+    d = irk.Integrator(irk.NBODY_DIRECT, 6 * 64, 0.1, 10, 1, params=[1.0, 0.01] + [1 / 64] * 64, exchange=1)
+    assert d.get_option(irk.OPT_EXCHANGE) == 1
+    d.close()
     w = irk.Integrator(irk.KEPLER, 4, -0.1, 10, 4, params=[1.0])  # negative h is allowed
     assert w.workspace_bytes == 64 + 8 * 8 * 4 * 4 + 8 * 4 * 4 + 4 * (256 + 2 * 4 + 1024)
     w.close()
