@@ -168,9 +168,11 @@ def run_reference(args):
             "warmup": args.warmup, "ms_per_step": 1e3 * T / args.steps, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "impl": "reference",
-            "config": {"workload": "config2_kepler_ensemble (sample)", "batch": S, "nsteps": w.nsteps},
+            "config": {"workload": "config2_kepler_ensemble", "batch_per_gpu": w.batch, "nsteps": w.nsteps,
+                       "h": w.h, "seed": wl.SEEDS[2]},
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle",
-                             "sample": f"first {S} of {w.batch} config-2 trajectories x {w.nsteps} steps per step"},
+                             "sample": f"first {S} of {w.batch} config-2 trajectories x {w.nsteps} steps per step "
+                                       "(the oracle as it stands, OpenMP over trajectories)"},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     return 0
