@@ -272,50 +272,71 @@ __global__ void nbd_or_kernel(const __grid_constant__ NbdArgs a) {
     a.ctl->nonfinite = bad;
 }
 
-// grid: x = local body tile (NBD_FORCE_THREADS bodies), y = stage i, z = j-block
-__global__ void __launch_bounds__(NBD_FORCE_THREADS) nbd_force_kernel(const __grid_constant__ NbdArgs a) {
-    __shared__ double4 sj[NBD_JBLOCK];
-    const int64_t N = a.nbody, nloc = a.nloc, dl = 3 * nloc;
-    const int i = blockIdx.y, J = blockIdx.z;
-    const int64_t j0 = (int64_t)J * NBD_JBLOCK;
-    const int nj = (int)((N - j0) < NBD_JBLOCK ? (N - j0) : NBD_JBLOCK);
-    double *cur = nbd_cur(a);
-    for (int t = threadIdx.x; t < nj; t += blockDim.x) {
-        const int64_t j = j0 + t;
-        const double *Qj = nbd_slot(a, cur, (int)(j / nloc)) + (int64_t)i * dl + 3 * (j % nloc);
-        sj[t] = make_double4(Qj[0], Qj[1], Qj[2], a.mass[j]);
-    }
-    __syncthreads();
-    const int64_t body = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;  // local index
-    if (body >= nloc) return;
-    const double *Qa = nbd_slot(a, cur, a.shard) + (int64_t)i * dl + 3 * body;
-    const double qx = Qa[0], qy = Qa[1], qz = Qa[2];
-    double px = 0.0, py = 0.0, pz = 0.0;
-    bool ok = true;
+// grid: x = local body tile (NBD_FORCE_THREADS bodies), y = stage i, z = j-block.
+// The j-block is staged through shared memory NBD_JSTAGE bodies at a time (the
+// thread's partial sum runs on across stages, so the j order -- and the bits --
+// are those of one pass over the block).
+#ifndef NBD_FORCE_MINB
+#define NBD_FORCE_MINB 1
+#endif
+#ifndef NBD_JSTAGE
+#define NBD_JSTAGE 1024
+#endif
+template <bool EXACT>
+__device__ __forceinline__ void nbd_pairs(const double4 *sj, int n, double qx, double qy, double qz, double G,
+                                          double eps2, double &px, double &py, double &pz, bool &ok) {
 #pragma unroll 4
-    for (int t = 0; t < nj; ++t) {
+    for (int t = 0; t < n; ++t) {
         const double4 pj = sj[t];
         const double dx = dsub(pj.x, qx), dy = dsub(pj.y, qy), dz = dsub(pj.z, qz);
-        const double r2 = dfma(dz, dz, dfma(dy, dy, dfma(dx, dx, a.eps2)));
-        const double w = ddiv_fast(a.G, dmul(r2, dsqrt_fast(r2, ok)), ok);
+        const double r2 = dfma(dz, dz, dfma(dy, dy, dfma(dx, dx, eps2)));
+        const double w = EXACT ? ddiv(G, dmul(r2, dsqrt(r2))) : ddiv_fast(G, dmul(r2, dsqrt_fast(r2, ok)), ok);
         const double s = dmul(pj.w, w);
         px = dfma(s, dx, px);
         py = dfma(s, dy, py);
         pz = dfma(s, dz, pz);
     }
-    if (!ok) {  // an operand outside the fast-path range: exact intrinsics, same bits
-        px = py = pz = 0.0;
-        for (int t = 0; t < nj; ++t) {
-            const double4 pj = sj[t];
-            const double dx = dsub(pj.x, qx), dy = dsub(pj.y, qy), dz = dsub(pj.z, qz);
-            const double r2 = dfma(dz, dz, dfma(dy, dy, dfma(dx, dx, a.eps2)));
-            const double w = ddiv(a.G, dmul(r2, dsqrt(r2)));
-            const double s = dmul(pj.w, w);
-            px = dfma(s, dx, px);
-            py = dfma(s, dy, py);
-            pz = dfma(s, dz, pz);
+}
+
+__global__ void __launch_bounds__(NBD_FORCE_THREADS, NBD_FORCE_MINB) nbd_force_kernel(const __grid_constant__ NbdArgs a) {
+    __shared__ double4 sj[NBD_JSTAGE];
+    const int64_t N = a.nbody, nloc = a.nloc, dl = 3 * nloc;
+    const int i = blockIdx.y, J = blockIdx.z;
+    const int64_t j0 = (int64_t)J * NBD_JBLOCK;
+    const int nj = (int)((N - j0) < NBD_JBLOCK ? (N - j0) : NBD_JBLOCK);
+    const double *cur = nbd_cur(a);
+    const int64_t body = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;  // local index
+    const bool act = body < nloc;
+    double qx = 0.0, qy = 0.0, qz = 0.0;
+    if (act) {
+        const double *Qa = nbd_slot(a, const_cast<double *>(cur), a.shard) + (int64_t)i * dl + 3 * body;
+        qx = Qa[0], qy = Qa[1], qz = Qa[2];
+    }
+    double px = 0.0, py = 0.0, pz = 0.0;
+    bool ok = true;
+    for (int pass = 0; pass < 2; ++pass) {  // pass 1 only if an operand left the fast-path range
+        for (int h0 = 0; h0 < nj; h0 += NBD_JSTAGE) {
+            const int nh = (nj - h0) < NBD_JSTAGE ? (nj - h0) : NBD_JSTAGE;
+            if (NBD_JSTAGE < NBD_JBLOCK || pass > 0) __syncthreads();  // the previous stage is consumed
+            for (int t = threadIdx.x; t < nh; t += blockDim.x) {
+                const int64_t j = j0 + h0 + t;
+                const double *Qj = nbd_slot(a, const_cast<double *>(cur), (int)(j / nloc)) + (int64_t)i * dl + 3 * (j % nloc);
+                sj[t] = make_double4(Qj[0], Qj[1], Qj[2], a.mass[j]);
+            }
+            __syncthreads();
+            if (act) {
+                if (pass == 0)
+                    nbd_pairs<false>(sj, nh, qx, qy, qz, a.G, a.eps2, px, py, pz, ok);
+                else
+                    nbd_pairs<true>(sj, nh, qx, qy, qz, a.G, a.eps2, px, py, pz, ok);
+            }
+        }
+        if (pass == 0) {  // exact intrinsics, same bits, for the whole block if any lane needs them
+            if (!__syncthreads_or(!ok)) break;
+            px = py = pz = 0.0;
         }
     }
+    if (!act) return;
     double *P = a.part + ((int64_t)J * 8 + i) * dl;
     P[3 * body] = px;
     P[3 * body + 1] = py;
