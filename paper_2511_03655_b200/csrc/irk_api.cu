@@ -1,6 +1,7 @@
 // C ABI of the IRKGL16 library (include/irk.h): context, workspace, dispatch.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cmath>
 #include <cstddef>
 #include <cstdarg>
@@ -337,7 +338,25 @@ int launch_direct(irk_ctx *c, double *y, double t0, char *ws, double *energy, in
         return cuda_check(c, cudaGetLastError(), "direct: frozen");
     }
     for (int t = 0; t < nlocal; ++t) irk::nbd_init_kernel<<<cb, 128, 0, st>>>(A[t]);
-    const dim3 fgrid((unsigned)((nloc + irk::NBD_FORCE_THREADS - 1) / irk::NBD_FORCE_THREADS), 8, (unsigned)nbd_nj(N));
+    const int nj = (int)nbd_nj(N);
+    auto force = [&](cudaStream_t s, const irk::NbdArgs &aa, int j_lo, int j_hi) {
+        if (j_hi <= j_lo) return;
+        const dim3 g((unsigned)((nloc + irk::NBD_FORCE_THREADS - 1) / irk::NBD_FORCE_THREADS), 8, (unsigned)(j_hi - j_lo));
+        irk::nbd_force_kernel<<<g, irk::NBD_FORCE_THREADS, 0, s>>>(aa, j_lo);
+    };
+    // Fused exchange: the j-blocks made only of this rank's bodies need no peer
+    // data, so they run before the arrival wait (overlapping the exchange, SURVEY
+    // 8(e)); the others after it.  Partial sums are per j-block, so the bits do
+    // not depend on the launch order.
+    int jl0 = 0, jl1 = 0;
+    if (fused) {
+        const int64_t b0 = A[0].b0, b1 = A[0].b0 + nloc;
+        jl0 = (int)((b0 + irk::NBD_JBLOCK - 1) / irk::NBD_JBLOCK);
+        jl1 = jl0;
+        while (jl1 < nj && (int64_t)jl1 * irk::NBD_JBLOCK >= b0 &&
+               std::min<int64_t>((int64_t)(jl1 + 1) * irk::NBD_JBLOCK, N) <= b1)
+            ++jl1;
+    }
     // one fixed-point sweep of every local shard (a2+a5, exchange, a3, a4+a6, counters)
     auto enqueue_sweep = [&](cudaStream_t s, cudaGraphConditionalHandle cond, int use_cond) -> int {
         for (int t = 0; t < nlocal; ++t) irk::nbd_pos_kernel<<<cb, 128, 0, s>>>(A[t]);
@@ -345,8 +364,14 @@ int launch_direct(irk_ctx *c, double *y, double t0, char *ws, double *energy, in
             int r = nccl_allgather_inplace(c, Qg, (size_t)stride, s);  // the exchange
             if (r) return r;
         }
+        if (fused) force(s, A[0], jl0, jl1);  // local x local, before the wait
         irk::nbd_or_kernel<<<1, 1, 0, s>>>(A[0]);
-        for (int t = 0; t < nlocal; ++t) irk::nbd_force_kernel<<<fgrid, irk::NBD_FORCE_THREADS, 0, s>>>(A[t]);
+        if (fused) {
+            force(s, A[0], 0, jl0);
+            force(s, A[0], jl1, nj);
+        } else {
+            for (int t = 0; t < nlocal; ++t) force(s, A[t], 0, nj);
+        }
         for (int t = 0; t < nlocal; ++t) irk::nbd_vel_kernel<<<cb, 128, 0, s>>>(A[t]);
         irk::nbd_ctl_kernel<<<1, 1, 0, s>>>(A[0], first, nlocal, n_done, stats, cond, use_cond);
         return cuda_check(c, cudaGetLastError(), "direct sweep launch");

@@ -298,10 +298,11 @@ __device__ __forceinline__ void nbd_pairs(const double4 *sj, int n, double qx, d
     }
 }
 
-__global__ void __launch_bounds__(NBD_FORCE_THREADS, NBD_FORCE_MINB) nbd_force_kernel(const __grid_constant__ NbdArgs a) {
+__global__ void __launch_bounds__(NBD_FORCE_THREADS, NBD_FORCE_MINB) nbd_force_kernel(const __grid_constant__ NbdArgs a,
+                                                                                      int jbase) {
     __shared__ double4 sj[NBD_JSTAGE];
     const int64_t N = a.nbody, nloc = a.nloc, dl = 3 * nloc;
-    const int i = blockIdx.y, J = blockIdx.z;
+    const int i = blockIdx.y, J = jbase + (int)blockIdx.z;  // j-blocks [jbase, jbase + gridDim.z)
     const int64_t j0 = (int64_t)J * NBD_JBLOCK;
     const int nj = (int)((N - j0) < NBD_JBLOCK ? (N - j0) : NBD_JBLOCK);
     const double *cur = nbd_cur(a);
