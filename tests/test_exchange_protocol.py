@@ -11,10 +11,11 @@ seeded random scheduler.  Per sweep of exchange epoch e, rank r:
   nbd_pos   reads its own Q^[k-1] from buffer (e+1)&1, stores Q^[k] into its slot
             of buffer e&1 in every rank's window, pushes its "not converged"
             vote into that buffer's flag, then its arrival word e+1 to every rank;
+  nbd_force the j-blocks of its own bodies (own slot of buffer e&1), then
   nbd_or    waits until every rank's arrival word (in its own window) is >= e+1,
             reads the flags of buffer e&1 from every slot, clears its own slot's
             flags of buffer (e+1)&1 in every window;
-  nbd_force reads every slot of buffer e&1;
+  nbd_force the other j-blocks: reads every slot of buffer e&1;
   nbd_vel   on divergence pushes its "non-finite" flag into buffer (e+1)&1;
   nbd_ctl   e <- e+1.
 and after a call's last sweep the final barrier (nbd_xfinal: arrive, wait, read
@@ -67,6 +68,9 @@ def run_protocol(P, calls, seed, double_buffer=True):
                 for p in range(P):
                     win[p]["arr"][r] = e + 1
                     yield
+                # nbd_force over the j-blocks of this rank's own bodies (before the wait)
+                check(win[r]["Q"].get((buf(e), r)) == ("Q", r, e), f"rank {r} local force at epoch {e}")
+                yield
                 # nbd_or
                 while not all(win[r]["arr"][s] >= e + 1 for s in range(P)):
                     yield "blocked"
