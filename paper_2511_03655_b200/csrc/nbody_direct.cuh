@@ -98,6 +98,9 @@ __device__ __forceinline__ double *nbd_cur(const NbdArgs &a) {
     return a.xmode ? a.Qg + (*nbd_xepoch(a) & 1) * a.qbuf : a.Qg;
 }
 __device__ __forceinline__ double *nbd_slot(const NbdArgs &a, double *buf, int s) { return buf + (int64_t)s * a.stride; }
+__device__ __forceinline__ const double *nbd_slot(const NbdArgs &a, const double *buf, int s) {
+    return buf + (int64_t)s * a.stride;
+}
 __device__ __forceinline__ double *nbd_slot(const NbdArgs &a, int s) { return nbd_slot(a, nbd_cur(a), s); }
 __device__ __forceinline__ int64_t nbd_flag_index(const NbdArgs &a) { return 24 * a.nloc; }
 // element o of this rank's slot in buffer b of rank r's window (NVLink store target)
@@ -310,7 +313,7 @@ __global__ void __launch_bounds__(NBD_FORCE_THREADS, NBD_FORCE_MINB) nbd_force_k
     const bool act = body < nloc;
     double qx = 0.0, qy = 0.0, qz = 0.0;
     if (act) {
-        const double *Qa = nbd_slot(a, const_cast<double *>(cur), a.shard) + (int64_t)i * dl + 3 * body;
+        const double *Qa = nbd_slot(a, cur, a.shard) + (int64_t)i * dl + 3 * body;
         qx = Qa[0], qy = Qa[1], qz = Qa[2];
     }
     double px = 0.0, py = 0.0, pz = 0.0;
@@ -321,7 +324,7 @@ __global__ void __launch_bounds__(NBD_FORCE_THREADS, NBD_FORCE_MINB) nbd_force_k
             if (NBD_JSTAGE < NBD_JBLOCK || pass > 0) __syncthreads();  // the previous stage is consumed
             for (int t = threadIdx.x; t < nh; t += blockDim.x) {
                 const int64_t j = j0 + h0 + t;
-                const double *Qj = nbd_slot(a, const_cast<double *>(cur), (int)(j / nloc)) + (int64_t)i * dl + 3 * (j % nloc);
+                const double *Qj = nbd_slot(a, cur, (int)(j / nloc)) + (int64_t)i * dl + 3 * (j % nloc);
                 sj[t] = make_double4(Qj[0], Qj[1], Qj[2], a.mass[j]);
             }
             __syncthreads();
