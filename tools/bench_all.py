@@ -64,9 +64,14 @@ def run(cfg, reps):
     sweeps = int(it.sum().item())
     steps = w.batch * w.nsteps
     fl = steps * 144 * d + sweeps * (280 * d + 8 * f_flops(w))
-    return {"config": cfg, "workload": w.name, "batch": w.batch, "nsteps": w.nsteps, "dim": w.dim,
-            "seconds": T, "traj_steps_per_s": steps / T, "sweeps_per_step": sweeps / steps,
-            "alg_tflops": fl / T / 1e12, "frac_fp64_peak": fl / T / PEAK, "times": ts, "rc": rc, **st}
+    out = {"config": cfg, "workload": w.name, "batch": w.batch, "nsteps": w.nsteps, "dim": w.dim,
+           "seconds": T, "traj_steps_per_s": steps / T, "sweeps_per_step": sweeps / steps,
+           "alg_tflops": fl / T / 1e12, "frac_fp64_peak": fl / T / PEAK, "times": ts, "rc": rc, **st}
+    if w.problem == wl.NBODY_DIRECT:  # one system -> system-steps/s and pair interactions/s
+        N = w.dim // 6
+        out["system_steps_per_s"] = w.nsteps / T
+        out["pair_interactions_per_s"] = float(N) * N * 8 * sweeps / T  # (i, j) incl. i = j (zero force), 8 stages
+    return out
 
 
 def main():
