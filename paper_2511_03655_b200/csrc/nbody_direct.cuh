@@ -276,69 +276,116 @@ __global__ void nbd_or_kernel(const __grid_constant__ NbdArgs a) {
 }
 
 // grid: x = local body tile (NBD_FORCE_THREADS bodies), y = stage i, z = j-block.
-// The j-block is staged through shared memory NBD_JSTAGE bodies at a time (the
-// thread's partial sum runs on across stages, so the j order -- and the bits --
-// are those of one pass over the block).
+// The j-block's positions and masses are staged in shared memory as packed
+// xyz[3 x 1024] and m[1024]: by two TMA bulk copies (cp.async.bulk, completion on
+// an mbarrier) when the block's bodies are contiguous in one slot of the gathered
+// buffer and 16-byte aligned -- every j-block of config 5 -- else by a gather.
+// The pair loop reads them as broadcast double2 loads, two bodies per trip, in j
+// order (the canonical per-block sum).
 #ifndef NBD_FORCE_MINB
 #define NBD_FORCE_MINB 1
 #endif
-#ifndef NBD_JSTAGE
-#define NBD_JSTAGE 1024
-#endif
 template <bool EXACT>
-__device__ __forceinline__ void nbd_pairs(const double4 *sj, int n, double qx, double qy, double qz, double G,
-                                          double eps2, double &px, double &py, double &pz, bool &ok) {
-#pragma unroll 4
-    for (int t = 0; t < n; ++t) {
-        const double4 pj = sj[t];
-        const double dx = dsub(pj.x, qx), dy = dsub(pj.y, qy), dz = dsub(pj.z, qz);
-        const double r2 = dfma(dz, dz, dfma(dy, dy, dfma(dx, dx, eps2)));
-        const double w = EXACT ? ddiv(G, dmul(r2, dsqrt(r2))) : ddiv_fast(G, dmul(r2, dsqrt_fast(r2, ok)), ok);
-        const double s = dmul(pj.w, w);
-        px = dfma(s, dx, px);
-        py = dfma(s, dy, py);
-        pz = dfma(s, dz, pz);
+__device__ __forceinline__ void nbd_pair(double xj, double yj, double zj, double mj, double qx, double qy, double qz,
+                                         double G, double eps2, double &px, double &py, double &pz, bool &ok) {
+    const double dx = dsub(xj, qx), dy = dsub(yj, qy), dz = dsub(zj, qz);
+    const double r2 = dfma(dz, dz, dfma(dy, dy, dfma(dx, dx, eps2)));
+    const double w = EXACT ? ddiv(G, dmul(r2, dsqrt(r2))) : ddiv_fast(G, dmul(r2, dsqrt_fast(r2, ok)), ok);
+    const double s = dmul(mj, w);
+    px = dfma(s, dx, px);
+    py = dfma(s, dy, py);
+    pz = dfma(s, dz, pz);
+}
+template <bool EXACT>
+__device__ __forceinline__ void nbd_pairs(const double *sxyz, const double *sm, int n, double qx, double qy, double qz,
+                                          double G, double eps2, double &px, double &py, double &pz, bool &ok) {
+    const double2 *x2 = reinterpret_cast<const double2 *>(sxyz);
+    const double2 *m2 = reinterpret_cast<const double2 *>(sm);
+#pragma unroll 2
+    for (int t2 = 0; t2 < n / 2; ++t2) {  // bodies 2 t2 and 2 t2 + 1
+        const double2 a0 = x2[3 * t2], a1 = x2[3 * t2 + 1], a2 = x2[3 * t2 + 2], mm = m2[t2];
+        nbd_pair<EXACT>(a0.x, a0.y, a1.x, mm.x, qx, qy, qz, G, eps2, px, py, pz, ok);
+        nbd_pair<EXACT>(a1.y, a2.x, a2.y, mm.y, qx, qy, qz, G, eps2, px, py, pz, ok);
     }
+    if (n & 1) {
+        const int t = n - 1;
+        nbd_pair<EXACT>(sxyz[3 * t], sxyz[3 * t + 1], sxyz[3 * t + 2], sm[t], qx, qy, qz, G, eps2, px, py, pz, ok);
+    }
+}
+
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
 
 __global__ void __launch_bounds__(NBD_FORCE_THREADS, NBD_FORCE_MINB) nbd_force_kernel(const __grid_constant__ NbdArgs a,
                                                                                       int jbase) {
-    __shared__ double4 sj[NBD_JSTAGE];
+    __shared__ __align__(128) double sxyz[3 * NBD_JBLOCK];
+    __shared__ __align__(16) double smass[NBD_JBLOCK];
+    __shared__ __align__(8) uint64_t mbar;
     const int64_t N = a.nbody, nloc = a.nloc, dl = 3 * nloc;
     const int i = blockIdx.y, J = jbase + (int)blockIdx.z;  // j-blocks [jbase, jbase + gridDim.z)
     const int64_t j0 = (int64_t)J * NBD_JBLOCK;
     const int nj = (int)((N - j0) < NBD_JBLOCK ? (N - j0) : NBD_JBLOCK);
     const double *cur = nbd_cur(a);
+    // ---- stage the j-block ----
+    const int s0 = (int)(j0 / nloc);
+    const double *src = nbd_slot(a, cur, s0) + (int64_t)i * dl + 3 * (j0 - (int64_t)s0 * nloc);
+    const double *msrc = a.mass + j0;
+    const bool bulk = ((j0 + nj - 1) / nloc == s0) && !(nj & 1) &&
+                      !((reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(msrc)) & 15);
+    if (bulk) {
+        if (threadIdx.x == 0) {
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&mbar)));
+            asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+            const uint32_t bx = 24u * (uint32_t)nj, bm = 8u * (uint32_t)nj;
+            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(&mbar)), "r"(bx + bm)
+                         : "memory");
+            asm volatile(
+                "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                    smem_u32(sxyz)),
+                "l"(src), "r"(bx), "r"(smem_u32(&mbar))
+                : "memory");
+            asm volatile(
+                "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                    smem_u32(smass)),
+                "l"(msrc), "r"(bm), "r"(smem_u32(&mbar))
+                : "memory");
+        }
+    } else {
+        for (int t = threadIdx.x; t < nj; t += blockDim.x) {
+            const int64_t j = j0 + t;
+            const double *Qj = nbd_slot(a, cur, (int)(j / nloc)) + (int64_t)i * dl + 3 * (j % nloc);
+            sxyz[3 * t] = Qj[0];
+            sxyz[3 * t + 1] = Qj[1];
+            sxyz[3 * t + 2] = Qj[2];
+            smass[t] = a.mass[j];
+        }
+    }
     const int64_t body = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;  // local index
     const bool act = body < nloc;
     double qx = 0.0, qy = 0.0, qz = 0.0;
-    if (act) {
+    if (act) {  // (overlaps the bulk copies)
         const double *Qa = nbd_slot(a, cur, a.shard) + (int64_t)i * dl + 3 * body;
         qx = Qa[0], qy = Qa[1], qz = Qa[2];
     }
+    __syncthreads();  // gather stores visible / mbarrier initialised before anyone waits on it
+    if (bulk) {
+        asm volatile(
+            "{\n"
+            ".reg .pred P1;\n"
+            "WAIT_%=:\n"
+            "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], 0;\n"
+            "@!P1 bra WAIT_%=;\n"
+            "}\n" ::"r"(smem_u32(&mbar))
+            : "memory");
+    }
+    // ---- the block's pair sums (pass 1 only if an operand left the fast-path range) ----
     double px = 0.0, py = 0.0, pz = 0.0;
     bool ok = true;
-    for (int pass = 0; pass < 2; ++pass) {  // pass 1 only if an operand left the fast-path range
-        for (int h0 = 0; h0 < nj; h0 += NBD_JSTAGE) {
-            const int nh = (nj - h0) < NBD_JSTAGE ? (nj - h0) : NBD_JSTAGE;
-            if (NBD_JSTAGE < NBD_JBLOCK || pass > 0) __syncthreads();  // the previous stage is consumed
-            for (int t = threadIdx.x; t < nh; t += blockDim.x) {
-                const int64_t j = j0 + h0 + t;
-                const double *Qj = nbd_slot(a, cur, (int)(j / nloc)) + (int64_t)i * dl + 3 * (j % nloc);
-                sj[t] = make_double4(Qj[0], Qj[1], Qj[2], a.mass[j]);
-            }
-            __syncthreads();
-            if (act) {
-                if (pass == 0)
-                    nbd_pairs<false>(sj, nh, qx, qy, qz, a.G, a.eps2, px, py, pz, ok);
-                else
-                    nbd_pairs<true>(sj, nh, qx, qy, qz, a.G, a.eps2, px, py, pz, ok);
-            }
-        }
-        if (pass == 0) {  // exact intrinsics, same bits, for the whole block if any lane needs them
-            if (!__syncthreads_or(!ok)) break;
-            px = py = pz = 0.0;
-        }
+    if (act) nbd_pairs<false>(sxyz, smass, nj, qx, qy, qz, a.G, a.eps2, px, py, pz, ok);
+    if (__syncthreads_or(!ok)) {  // exact intrinsics, same bits, for the whole block
+        px = py = pz = 0.0;
+        if (act) nbd_pairs<true>(sxyz, smass, nj, qx, qy, qz, a.G, a.eps2, px, py, pz, ok);
     }
     if (!act) return;
     double *P = a.part + ((int64_t)J * 8 + i) * dl;
