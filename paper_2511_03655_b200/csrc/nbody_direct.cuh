@@ -17,13 +17,14 @@
 //                         collective -- nbd_pos stores each Q^[k] value straight into
 //                         every rank's copy of its slot (NVLink peer pointers of a
 //                         symmetric NCCL window) and its last CTA signals arrival to
-//                         every rank; see "Fused exchange" below.
+//                         every rank; see the fused-exchange helpers below.
 //   nbd_or                global stop = no flag set in any slot (same on every rank);
-//                         fused mode: first waits for every rank's arrival.
+//                         fused mode: first waits for every rank's arrival (the
+//                         j-blocks of the rank's own bodies are summed before it).
 //   nbd_force  (a3)       (local body, stage, j-block) parallel: the canonical blocked
 //                         direct sum (R-8) over ALL N bodies read from Qg,
 //                         one thread = one partial sum over NBD_JBLOCK = 1024 bodies j
-//                         staged in shared memory (broadcast reads).
+//                         staged in shared memory by TMA bulk copies (broadcast reads).
 //   nbd_vel    (a4 + a6)  acc = ((0 + P_0) + P_1) + ... , Lv = hb o acc, then
 //                         V = v + D(mu, Lv) or (converged) update + history + nu-init.
 //   nbd_ctl    (1 thread) sweep / step counters (identical decisions on all ranks).
