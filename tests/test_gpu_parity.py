@@ -560,10 +560,13 @@ def test_config5_plummer_small_full_length_energy(irk, orc):
     assert_parity(g, o, energy=True)
 
 
-def test_config5_ragged_blocks(irk, orc):
-    """N = 2,500: three canonical j-blocks, the last one partial; 25 steps."""
-    w = wl.plummer(N=2500, nsteps=25)
-    g = run_gpu(irk, w, chunks=5)
+@pytest.mark.parametrize("N,nsteps,chunks", [(2500, 25, 5), (1025, 6, 2), (1023, 6, 1)])
+def test_config5_ragged_blocks(irk, orc, N, nsteps, chunks):
+    """Ragged j-blocks: N = 2,500 (three blocks, the last partial, TMA-staged);
+    N = 1,025 (a one-body last block: odd, so gathered instead of bulk-copied);
+    N = 1,023 (one odd block, gathered)."""
+    w = wl.plummer(N=N, nsteps=nsteps)
+    g = run_gpu(irk, w, chunks=chunks)
     o = orc.integrate(w.problem, w.y, w.params, w.h, w.nsteps)
     assert_parity(g, o)
 
