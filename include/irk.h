@@ -71,7 +71,9 @@ enum irk_option {
                                  trajectory, one stage per lane (warp-shuffle contractions and
                                  convergence reduction).  IRK_NBODY: IRK_MAP_G1 = body per lane,
                                  IRK_MAP_G8 = stage per lane (shared-memory all-gather).  Auto
-                                 picks by batch size.  Bitwise-neutral.  */
+                                 picks by problem, N and batch size from measured crossovers
+                                 (the chunked IRK_OPT_SCHEDULE = 1 keeps
+                                 body per lane).  Bitwise-neutral.  */
     IRK_OPT_BALANCE = 5,      /* ensemble scheduling: -1 = auto (default), 0 = off, C > 0 = run the
                                  call in chunks of C steps, re-sorting trajectories by the cost of
                                  the previous chunk (bitwise-neutral)  */

@@ -45,10 +45,15 @@ __device__ __forceinline__ void n8_accel(const double *Q, double *A, const NBody
                                          bool &ok) {
     constexpr int NP = NB * (NB - 1) / 2;
     double w[NP];
+    // constant trip counts and a closed-form pair index: fully unrolled, so Q and w
+    // stay in registers (a triangular loop with a running index was not unrolled and
+    // put Q in local memory)
 #pragma unroll
-    for (int i = 0, p = 0; i < NB; ++i)
+    for (int i = 0; i < NB; ++i)
 #pragma unroll
-        for (int j = i + 1; j < NB; ++j, ++p) {
+        for (int j = 0; j < NB; ++j) {
+            if (j <= i) continue;
+            const int p = i * NB - i * (i + 1) / 2 + (j - i - 1);
             const double dx = dsub(Q[3 * j], Q[3 * i]), dy = dsub(Q[3 * j + 1], Q[3 * i + 1]),
                          dz = dsub(Q[3 * j + 2], Q[3 * i + 2]);
             const double r2 = dfma(dz, dz, dfma(dy, dy, dfma(dx, dx, P.eps2)));
@@ -73,6 +78,20 @@ __device__ __forceinline__ void n8_accel(const double *Q, double *A, const NBody
         A[3 * i + 1] = ay;
         A[3 * i + 2] = az;
     }
+}
+
+// The exact-intrinsic re-evaluation (rare: an operand outside the div/sqrt fast
+// path) through the lane's own tile row, out of line: called on the registers Q,
+// F directly it made ptxas keep both arrays addressable in local memory on the
+// hot path too.
+template <int NB>
+__device__ __noinline__ void n8_accel_exact_row(double *row, const NBodyParams &P, const double *sm) {
+    constexpr int d = 3 * NB;
+    double Q[d], F[d];
+    bool ok = true;
+    for (int l = 0; l < d; ++l) Q[l] = row[l];
+    n8_accel<NB, true>(Q, F, P, sm, ok);
+    for (int l = 0; l < d; ++l) row[l] = F[l];
 }
 
 template <int NB>
@@ -247,7 +266,13 @@ __global__ void __maxnreg__(N8_MAXREG) ens_nbody8_kernel(const __grid_constant__
             double F[d];
             bool ok = true;
             n8_accel<NB, false>(Q, F, P, sm, ok);
-            if (!ok) n8_accel<NB, true>(Q, F, P, sm, ok);  // exact intrinsics, same bits
+            if (!ok) {  // exact intrinsics, same bits (row s of T is free until the Lv store below)
+#pragma unroll
+                for (int l = 0; l < d; ++l) T[s * DP + l] = Q[l];
+                n8_accel_exact_row<NB>(&T[s * DP], P, sm);
+#pragma unroll
+                for (int l = 0; l < d; ++l) F[l] = T[s * DP + l];
+            }
 #pragma unroll
             for (int l = 0; l < d; ++l) T[s * DP + l] = dmul(hb_s, F[l]);
         }

@@ -71,7 +71,6 @@ namespace {
 
 constexpr size_t kHeader = 64;
 constexpr int64_t kG8AutoMaxBatch = 12288;  // IRK_OPT_MAPPING auto: g8 up to this batch (Kepler, HH)
-constexpr int64_t kN8AutoMaxBatch = 6144;       // IRK_OPT_MAPPING auto: stage-per-lane N-body up to this batch
 constexpr int64_t kFo8AutoMaxBatch = INT64_MAX;  // first-order mode: stage per lane at every measured batch
                                                  // (tools/fo_bench.py: 1 to 65,536 trajectories)
 
@@ -550,6 +549,20 @@ int launch_g8(irk_ctx *c, const P &prob, EnsArgs &a, char *ws, cudaStream_t st) 
     return cuda_check(c, cudaGetLastError(), "advance_n launch");
 }
 
+// IRK_OPT_MAPPING auto for the N-body ensembles: stage per lane (ens_nbody8) where
+// tools/nb_map_ab.py measured it faster than body per lane (1,000 steps, batches
+// 2,048 / 6,144 / 16,384 / 65,536; profiles/r1/nb_map_ab.json): N = 3, 4, 6 at every
+// batch (config 3: 40.6 vs 45.8 ms at 16,384); N = 2 up to 16,384; N = 5 up to
+// 6,144; N = 8 except near 6,144.
+bool nbody8_auto(int NB, int64_t batch) {
+    switch (NB) {
+    case 2: return batch <= 32768;
+    case 5: return batch <= 8192;
+    case 8: return batch <= 4096 || batch >= 12288;
+    default: return true;
+    }
+}
+
 // IRK_OPT_MAPPING auto for the per-thread problems: g8 while the batch leaves
 // most g1 lanes of the GPU empty (measured crossover).
 bool use_g8(const irk_ctx *c) {
@@ -610,10 +623,9 @@ int launch_nbody_t(irk_ctx *c, double *y, double t0, char *ws, double *energy, i
     EnsArgs a = ens_args(c, y, t0, ws, energy, iters);
     constexpr int GPW = 32 / NB, WPB = irk::NB_THREADS / 32;
     const int64_t blocks = (c->batch + GPW * WPB - 1) / (GPW * WPB);
-    // stage-per-lane (ensemble_nbody8.cuh) when asked, or (auto) while the batch is too small to
-    // fill the GPU with body-per-lane groups (config-3 generator, 2,000 steps: 1.25x faster at
-    // 512-4,096 trajectories, equal at 8,192, 0.79x at 16,384)
-    if (c->mapping == IRK_MAP_G8 || (c->mapping == IRK_MAP_AUTO && c->batch <= kN8AutoMaxBatch))
+    // stage-per-lane (ensemble_nbody8.cuh) when asked or where auto measured it faster; the
+    // chunked schedule (IRK_OPT_SCHEDULE = 1) keeps body-per-lane
+    if (c->mapping == IRK_MAP_G8 || (c->mapping == IRK_MAP_AUTO && c->schedule != 1 && nbody8_auto(NB, c->batch)))
         return launch_queue(c, irk::ens_nbody8_kernel<NB>, irk::N8_THREADS, irk::N8_THREADS / 8,
                             &c->nbody8_blocks_per_sm[NB], a, ws, st,
                             [&](const EnsArgs &aa, const irk::QueueArgs &qa, unsigned nb) {

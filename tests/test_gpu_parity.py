@@ -27,14 +27,14 @@ def irk():
     return irk
 
 
-def run_gpu(irk, w, y=None, nsteps=None, energy_every=0, max_iters=100, chunks=1, t0=0.0):
+def run_gpu(irk, w, y=None, nsteps=None, energy_every=0, max_iters=100, chunks=1, t0=0.0, mapping=0):
     y = w.y if y is None else y
     nsteps = w.nsteps if nsteps is None else nsteps
     assert nsteps % chunks == 0
     per = nsteps // chunks
     B = y.shape[1]
     with irk.Integrator(w.problem, w.dim, w.h, per, B, w.params, energy_every=energy_every,
-                        max_iters=max_iters) as ig:
+                        max_iters=max_iters, mapping=mapping) as ig:
         Y = torch.tensor(y, dtype=torch.float64, device="cuda").contiguous()
         ws = ig.new_workspace()
         it_total = torch.zeros(B, dtype=torch.int64, device="cuda")
@@ -383,12 +383,14 @@ def test_work_queue_nbody_bitwise(irk, orc):
     slots + a partial one), more warp slots than resident warps, units of 13
     steps, energy samples and Delta H^loc across units; equal to the single
     launch, to the chunked cost-sorted launches (whose permutation once overran
-    its buffer for this mapping) and to the oracle."""
+    its buffer for this mapping), to the stage-per-lane queue kernel (the auto
+    mapping at this batch) and to the oracle."""
     w = wl.six_body_ensemble(batch=16384, nsteps=130)
     outs = []
-    for sched, bal in ((1, 0), (2, 13), (1, 26)):  # (1, 26): chunked + cost-sorted permutation
+    # (1, 26): chunked + cost-sorted permutation; mapping 8: stage per lane (ens_nbody8)
+    for sched, bal, mp in ((1, 0, 1), (2, 13, 1), (1, 26, 1), (2, 13, 8), (0, -1, 0)):
         with irk.Integrator(w.problem, w.dim, w.h, w.nsteps, w.batch, w.params, energy_every=26,
-                            balance=bal, schedule=sched, local_energy=True) as ig:
+                            balance=bal, schedule=sched, local_energy=True, mapping=mp) as ig:
             Y = torch.tensor(w.y, dtype=torch.float64, device="cuda")
             ws = ig.new_workspace()
             E = torch.zeros((ig.n_energy(), w.batch), dtype=torch.float64, device="cuda")
@@ -486,17 +488,18 @@ def test_config3_full_batch_sampled(irk, orc):
     assert_parity(dict(y=g["y"][:, idx], iters=g["iters"][idx]), o)
 
 
-def test_nbody_small_n_variants(irk, orc):
-    """Other group sizes of the body-per-lane kernel (N = 2, 3, 5): random
-    softened systems, bitwise."""
+@pytest.mark.parametrize("mapping", [1, 8])
+def test_nbody_small_n_variants(irk, orc, mapping):
+    """Other N of both N-body mappings (N = 2, 3, 4, 5, 8; body per lane and
+    stage per lane): random softened systems, bitwise."""
     rng = np.random.default_rng(3)
-    for N in (2, 3, 5):
+    for N in (2, 3, 4, 5, 8):
         B = 23
         q = rng.standard_normal((3 * N, B))
         v = 0.3 * rng.standard_normal((3 * N, B))
         params = np.concatenate([[1.0, 0.05], rng.uniform(0.2, 1.0, N)])
         w = wl.Workload(f"nb{N}", wl.NBODY, 6 * N, np.concatenate([q, v]), params, 0.01, 300)
-        g = run_gpu(irk, w, energy_every=100)
+        g = run_gpu(irk, w, energy_every=100, mapping=mapping)
         o = orc.integrate(w.problem, w.y, w.params, w.h, w.nsteps, energy_every=100)
         assert_parity(g, o, energy=True)
 

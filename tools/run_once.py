@@ -17,6 +17,7 @@ ap.add_argument("--reps", type=int, default=1)
 ap.add_argument("--host-loop", action="store_true", help="config 5: host-driven sweep loop (ncu sees each kernel)")
 ap.add_argument("--comm", action="store_true", help="config 5: 1-rank NCCL communicator")
 ap.add_argument("--exchange", type=int, default=0, help="config 5 with --comm: IRK_OPT_EXCHANGE")
+ap.add_argument("--mapping", type=int, default=0, help="IRK_OPT_MAPPING (0 auto, 1 g1 / body per lane, 8 stage per lane)")
 a = ap.parse_args()
 kw = {}
 if a.batch:
@@ -27,6 +28,8 @@ w = wl.config(a.config, **kw)
 kw2 = {"device_loop": 0} if (a.host_loop and w.problem == wl.NBODY_DIRECT) else {}
 if a.exchange:
     kw2["exchange"] = a.exchange
+if a.mapping:
+    kw2["mapping"] = a.mapping
 with irk.Integrator(w.problem, w.dim, w.h, w.nsteps, w.batch, w.params, **kw2) as ig:
     if a.comm:
         ig.set_comm(irk.nccl_unique_id(), 0, 1)

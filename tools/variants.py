@@ -29,6 +29,7 @@ def build_all():
 CFG = int(os.environ.get("IRK_VARIANT_CONFIG", "2"))
 NSTEPS = int(os.environ.get("IRK_VARIANT_NSTEPS", "0"))
 SCHED = int(os.environ.get("IRK_VARIANT_SCHEDULE", "0"))
+MAPPING = int(os.environ.get("IRK_VARIANT_MAPPING", "0"))
 
 
 def time_one(name):
@@ -39,7 +40,7 @@ os.environ['IRK_LIB_OVERRIDE'] = {lib!r}
 sys.path.insert(0, {ROOT!r})
 from paper_2511_03655_b200 import irk, workloads as wl
 w = wl.config({CFG}, **({{'nsteps': {NSTEPS}}} if {NSTEPS} else {{}}))
-ig = irk.Integrator(w.problem, w.dim, w.h, w.nsteps, w.batch, w.params, schedule={SCHED})
+ig = irk.Integrator(w.problem, w.dim, w.h, w.nsteps, w.batch, w.params, schedule={SCHED}, mapping={MAPPING})
 y0 = torch.tensor(w.y, device='cuda'); Y = torch.empty_like(y0); ws = ig.new_workspace()
 ts = []
 for r in range(4):
