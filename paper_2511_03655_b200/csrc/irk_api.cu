@@ -938,7 +938,6 @@ int irk_set_option(irk_ctx *c, int key, int64_t val) {
     case IRK_OPT_EXCHANGE:
         if (c->problem != IRK_NBODY_DIRECT || (val != 0 && val != 1))
             return fail(c, IRK_E_ARG, "irk_set_option: EXCHANGE is 0 or 1, for IRK_NBODY_DIRECT");
-        if (c->xwin && val != 1) return fail(c, IRK_E_STATE, "irk_set_option: the fused exchange window is in use");
         c->exchange = (int)val;
         return IRK_OK;
     case IRK_OPT_DEVICE_LOOP:
