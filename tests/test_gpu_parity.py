@@ -709,6 +709,25 @@ def test_config5_fused_exchange_single_rank(irk, orc, device_loop):
     assert g["iters"] == int(o["iters"][0]) and g["rc"] == irk.OK
 
 
+def test_config5_exchange_switch_between_calls(irk, orc):
+    """IRK_OPT_EXCHANGE switched 1 -> 0 -> 1 between chained calls (the window
+    stays allocated while the all-gather runs): still the oracle's bits."""
+    try:
+        uid = irk.nccl_unique_id()
+    except irk.IrkError:
+        pytest.skip("NCCL not loadable")
+    w = wl.plummer(N=512, nsteps=3)
+    o = orc.integrate(w.problem, w.y, w.params, w.h, 9)
+    with irk.Integrator(w.problem, w.dim, w.h, w.nsteps, 1, w.params, exchange=1) as ig:
+        ig.set_comm(uid, 0, 1)
+        Y = torch.tensor(w.y, dtype=torch.float64, device="cuda")
+        ws = ig.new_workspace()
+        for ex in (1, 0, 1):
+            ig.set_option(irk.OPT_EXCHANGE, ex)
+            ig.integrate(Y, ws)
+        assert np.array_equal(Y.cpu().numpy(), o["y"])
+
+
 def test_config5_fused_exchange_divergence(irk):
     """A non-finite body: the divergence flag travels through the fused exchange
     (nbd_vel's store into the next buffer, the final barrier) exactly as through
