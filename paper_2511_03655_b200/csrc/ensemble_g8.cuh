@@ -37,27 +37,32 @@ constexpr int G8_THREADS = 64;  // 8 trajectories per block
 #define G8_MAXREG 128  // config-2 generator, 2,000 steps, B = 2048: 80 regs 5.8 ms, 96: 5.2, 128: 4.7 (g1: 8.7)
 #endif
 
-template <class P>
-__global__ void __maxnreg__(G8_MAXREG) ens_g8_kernel(const __grid_constant__ EnsArgs a,
-                                                            const __grid_constant__ P prob) {
-    constexpr int d = P::d, D = 2 * d;
+// G lanes per trajectory (G = 8: "g8", one stage per lane; G = 4: "g4", two
+// stages per lane -- half the lanes and half the replicated work per trajectory,
+// for batches too large for g8 and too small for g1).  Lane s of a group owns
+// stages s*SPL .. s*SPL + SPL - 1.
+template <class P, int G>
+__global__ void __maxnreg__(G8_MAXREG) ens_gs_kernel(const __grid_constant__ EnsArgs a,
+                                                     const __grid_constant__ P prob) {
+    static_assert(G == 8 || G == 4, "G lanes per trajectory: 8 or 4");
+    constexpr int d = P::d, D = 2 * d, SPL = 8 / G, GPB = G8_THREADS / G;
     const unsigned FULL = 0xffffffffu;
     const int64_t B = a.batch;
-    const int lane = threadIdx.x & 31, s = lane & 7, base = lane & ~7;
-    const int64_t b = ((int64_t)blockIdx.x * G8_THREADS + threadIdx.x) >> 3;  // trajectory of the group
+    const int lane = threadIdx.x & 31, s = lane & (G - 1), base = lane & ~(G - 1);
+    const int64_t b = ((int64_t)blockIdx.x * G8_THREADS + threadIdx.x) / G;  // trajectory of the group
     const bool valid = b < B;
     const int64_t bb = valid ? b : 0;
 
-    // Lane-dependent coefficients from shared memory, column-major [j][s] so that
-    // the 8 lanes of a group read 8 consecutive doubles (all groups of the warp
-    // the same ones); nu~ offset by 72 doubles to sit in other banks than mu~.
+    // Lane-dependent coefficients from shared memory, column-major [j][i] so that
+    // the lanes of a group read consecutive doubles (all groups of the warp the
+    // same ones); nu~ offset by 72 doubles to sit in other banks than mu~.
     // (Kept in registers they were rematerialised from the constant bank with
     // lane-divergent addresses: serialised LDC, ncu mio_throttle.)
     __shared__ double sW[72 + 64], sHB[8], sC[8];
 #if G8_SMEM
     // per-group all-gather tile [stage][component], groups padded into different banks
-    __shared__ __align__(16) double sG[G8_THREADS / 8][8 * d + 2];
-    const int gib = threadIdx.x >> 3;
+    __shared__ __align__(16) double sG[GPB][8 * d + 2];
+    const int gib = threadIdx.x / G;
 #endif
     for (int e = threadIdx.x; e < 64; e += blockDim.x) {
         sW[(e & 7) * 8 + (e >> 3)] = (&c_mu[0][0])[e];       // mu~[i][j] at [j][i]
@@ -68,7 +73,8 @@ __global__ void __maxnreg__(G8_MAXREG) ens_g8_kernel(const __grid_constant__ Ens
         sC[threadIdx.x] = c_c[threadIdx.x];
     }
     __syncthreads();
-    const double *Mu = sW + s, *Nu = sW + 72 + s;  // coefficient (s, j) at [8 j]
+    const int st0 = s * SPL;                           // first owned stage
+    const double *Mu = sW + st0, *Nu = sW + 72 + st0;  // coefficient (st0 + t, j) at [8 j + t]
 
     double q[d], v[d];
 #pragma unroll
@@ -91,66 +97,89 @@ __global__ void __maxnreg__(G8_MAXREG) ens_g8_kernel(const __grid_constant__ Ens
         if (a.local_energy && a.c0 == 0) a.stats[3 * B + b] = 0;
     }
 
-    // a1: V_s = v + D(nu_s., H), H = the history rows of all 8 stages
-    double Vs[d];
+    // a1: V_i = v + D(nu_i., H) for the owned stages, H = the history rows of all 8 stages
+    double Vs[SPL][d];
     {
-        double Hs[d];
+        double Hs[SPL][d];
 #pragma unroll
-        for (int l = 0; l < d; ++l) Hs[l] = live ? a.hist[((int64_t)s * D + d + l) * B + b] : 0.0;
+        for (int t = 0; t < SPL; ++t)
+#pragma unroll
+            for (int l = 0; l < d; ++l) Hs[t][l] = live ? a.hist[((int64_t)(st0 + t) * D + d + l) * B + b] : 0.0;
 #pragma unroll
         for (int l = 0; l < d; ++l) {
-            double acc = dmul(Nu[0], __shfl_sync(FULL, Hs[l], base));
+            double H[8];
 #pragma unroll
-            for (int j = 1; j < 8; ++j) acc = dfma(Nu[8 * j], __shfl_sync(FULL, Hs[l], base + j), acc);
-            Vs[l] = dadd(v[l], acc);
+            for (int j = 0; j < 8; ++j) H[j] = __shfl_sync(FULL, Hs[j % SPL][l], base + j / SPL);
+#pragma unroll
+            for (int t = 0; t < SPL; ++t) {
+                double acc = dmul(Nu[t], H[0]);
+#pragma unroll
+                for (int j = 1; j < 8; ++j) acc = dfma(Nu[8 * j + t], H[j], acc);
+                Vs[t][l] = dadd(v[l], acc);
+            }
         }
     }
     constexpr int64_t kInfBits = 0x7ff0000000000000LL;
     int64_t m[d], p[d];
-    double Qold[d];
+    double Qold[SPL][d];
 #pragma unroll
     for (int l = 0; l < d; ++l) {
         m[l] = p[l] = kInfBits;
-        Qold[l] = 0.0;
+#pragma unroll
+        for (int t = 0; t < SPL; ++t) Qold[t][l] = 0.0;
     }
     int64_t n = 0, hits = 0, sweeps = 0;
     int k = 0;
     while (__any_sync(FULL, live)) {  // warp-uniform: every lane takes part in the shuffles
         ++k;
         // ---- a2 + a5 ----
-        double sLq[d], Qs[d];  // S(Lq) is formed on the fly (the gathered Lq die here)
+        double sLq[d], Qs[SPL][d];  // S(Lq) is formed on the fly (the gathered Lq die here)
         bool stop = (k >= 2);
-        const double hb_s = sHB[s];
-#pragma unroll
 #if G8_SMEM
-        for (int l = 0; l < d; ++l) sG[gib][s * d + l] = dmul(hb_s, Vs[l]);
+#pragma unroll
+        for (int t = 0; t < SPL; ++t)
+#pragma unroll
+            for (int l = 0; l < d; ++l) sG[gib][(st0 + t) * d + l] = dmul(sHB[st0 + t], Vs[t][l]);
         __syncwarp();
+#else
+        static_assert(G == 8, "the shuffle all-gather is written for one stage per lane");
+        double lq[d];
+#pragma unroll
+        for (int l = 0; l < d; ++l) lq[l] = dmul(sHB[s], Vs[0][l]);
 #endif
+#pragma unroll
         for (int l = 0; l < d; ++l) {
 #if G8_SMEM
             double g = sG[gib][l];
 #else
-            const double lq = dmul(hb_s, Vs[l]);
-            double g = __shfl_sync(FULL, lq, base);
+            double g = __shfl_sync(FULL, lq[l], base);
 #endif
-            double acc = dmul(Mu[0], g);
+            double acc[SPL];
+#pragma unroll
+            for (int t = 0; t < SPL; ++t) acc[t] = dmul(Mu[t], g);
             sLq[l] = g;
 #pragma unroll
             for (int j = 1; j < 8; ++j) {
 #if G8_SMEM
                 g = sG[gib][j * d + l];
 #else
-                g = __shfl_sync(FULL, lq, base + j);
+                g = __shfl_sync(FULL, lq[l], base + j);
 #endif
-                acc = dfma(Mu[8 * j], g, acc);
+#pragma unroll
+                for (int t = 0; t < SPL; ++t) acc[t] = dfma(Mu[8 * j + t], g, acc[t]);
                 sLq[l] = dadd(sLq[l], g);
             }
-            Qs[l] = dadd(q[l], acc);
-            int64_t e = __double_as_longlong(dsub(Qs[l], Qold[l])) & 0x7fffffffffffffffLL;
-            e = (e > kInfBits) ? 0 : e;  // NaN-ignoring max (canonical left-to-right form)
-            Qold[l] = Qs[l];
+            int64_t e = 0;
 #pragma unroll
-            for (int off = 1; off < 8; off <<= 1) {
+            for (int t = 0; t < SPL; ++t) {
+                Qs[t][l] = dadd(q[l], acc[t]);
+                int64_t et = __double_as_longlong(dsub(Qs[t][l], Qold[t][l])) & 0x7fffffffffffffffLL;
+                et = (et > kInfBits) ? 0 : et;  // NaN-ignoring max (canonical left-to-right form)
+                e = (et > e) ? et : e;
+                Qold[t][l] = Qs[t][l];
+            }
+#pragma unroll
+            for (int off = 1; off < G; off <<= 1) {
                 const int64_t o = __shfl_xor_sync(FULL, e, off);
                 e = (o > e) ? o : e;
             }
@@ -162,21 +191,27 @@ __global__ void __maxnreg__(G8_MAXREG) ens_g8_kernel(const __grid_constant__ Ens
                 stop = stop && ok;
             }
         }
-        // ---- a3: one right-hand side per lane ----
+        // ---- a3: SPL right-hand sides per lane ----
         const double tn1 = dadd(a.t0, dmul((double)(n0 + n), a.h));
-        const double ts = dadd(tn1, dmul(sC[s], a.h));
-        double Fs[d];
+        double Fs[SPL][d];
         {
             bool ok = true;
-            prob.template accel<false>(Qs, Fs, ts, ok);
-            if (!ok) prob.template accel<true>(Qs, Fs, ts, ok);  // exact slow path, same bits
+#pragma unroll
+            for (int t = 0; t < SPL; ++t)
+                prob.template accel<false>(Qs[t], Fs[t], dadd(tn1, dmul(sC[st0 + t], a.h)), ok);
+            if (!ok)  // exact slow path, same bits
+#pragma unroll
+                for (int t = 0; t < SPL; ++t)
+                    prob.template accel<true>(Qs[t], Fs[t], dadd(tn1, dmul(sC[st0 + t], a.h)), ok);
         }
         // ---- a4 (first half): Lv, all-gather ----
-        double Lvg[8][d], Lvs[d];
+        double Lvg[8][d], Lvs[SPL][d];
 #if G8_SMEM
         __syncwarp();  // the Lq reads of this sweep are done
 #pragma unroll
-        for (int l = 0; l < d; ++l) sG[gib][s * d + l] = Lvs[l] = dmul(sHB[s], Fs[l]);
+        for (int t = 0; t < SPL; ++t)
+#pragma unroll
+            for (int l = 0; l < d; ++l) sG[gib][(st0 + t) * d + l] = Lvs[t][l] = dmul(sHB[st0 + t], Fs[t][l]);
         __syncwarp();
 #pragma unroll
         for (int j = 0; j < 8; ++j)
@@ -186,9 +221,9 @@ __global__ void __maxnreg__(G8_MAXREG) ens_g8_kernel(const __grid_constant__ Ens
 #else
 #pragma unroll
         for (int l = 0; l < d; ++l) {
-            Lvs[l] = dmul(sHB[s], Fs[l]);
+            Lvs[0][l] = dmul(sHB[s], Fs[0][l]);
 #pragma unroll
-            for (int j = 0; j < 8; ++j) Lvg[j][l] = __shfl_sync(FULL, Lvs[l], base + j);
+            for (int j = 0; j < 8; ++j) Lvg[j][l] = __shfl_sync(FULL, Lvs[0][l], base + j);
         }
 #endif
         const bool fin = live && (stop || k >= a.max_iters);
@@ -214,26 +249,30 @@ __global__ void __maxnreg__(G8_MAXREG) ens_g8_kernel(const __grid_constant__ Ens
                     a.energy[((a.c0 + n) / a.energy_every) * B + b] = prob.energy(q, v);
                 if (a.local_energy) dhloc_update(prob.energy(q, v), hprev, dhmax);
             }
-            if (n == a.nsteps || !finite) {  // leave: history row s = Lv_s, q block zeroed (R-4)
+            if (n == a.nsteps || !finite) {  // leave: history rows = Lv of the owned stages, q block zeroed (R-4)
 #pragma unroll
-                for (int l = 0; l < d; ++l) {
-                    a.hist[((int64_t)s * D + l) * B + b] = 0.0;
-                    a.hist[((int64_t)s * D + d + l) * B + b] = Lvs[l];
-                }
+                for (int t = 0; t < SPL; ++t)
+#pragma unroll
+                    for (int l = 0; l < d; ++l) {
+                        a.hist[((int64_t)(st0 + t) * D + l) * B + b] = 0.0;
+                        a.hist[((int64_t)(st0 + t) * D + d + l) * B + b] = Lvs[t][l];
+                    }
                 if (!finite) bad = n0 + n;
                 live = false;
             }
         }
-        // ---- a4 (second half) / next step's a1: V_s = v + D(W_s., Lv) ----
+        // ---- a4 (second half) / next step's a1: V_i = v + D(W_i., Lv) ----
         {
             const double *W = fin ? Nu : Mu;
 #pragma unroll
-            for (int l = 0; l < d; ++l) {
-                double acc = dmul(W[0], Lvg[0][l]);
+            for (int l = 0; l < d; ++l)
 #pragma unroll
-                for (int j = 1; j < 8; ++j) acc = dfma(W[8 * j], Lvg[j][l], acc);
-                Vs[l] = dadd(v[l], acc);
-            }
+                for (int t = 0; t < SPL; ++t) {
+                    double acc = dmul(W[t], Lvg[0][l]);
+#pragma unroll
+                    for (int j = 1; j < 8; ++j) acc = dfma(W[8 * j + t], Lvg[j][l], acc);
+                    Vs[t][l] = dadd(v[l], acc);
+                }
         }
     }
     if (valid && s == 0) {

@@ -70,7 +70,17 @@ struct irk_ctx {
 namespace {
 
 constexpr size_t kHeader = 64;
-constexpr int64_t kG8AutoMaxBatch = 12288;  // IRK_OPT_MAPPING auto: g8 up to this batch (Kepler, HH)
+#ifndef IRK_G8_AUTO_MAX
+#define IRK_G8_AUTO_MAX 6144
+#endif
+#ifndef IRK_G4_AUTO_MAX
+#define IRK_G4_AUTO_MAX 16384
+#endif
+// IRK_OPT_MAPPING auto (Kepler, HH): g8 up to kG8AutoMaxBatch, then g4 up to kG4AutoMaxBatch, then g1
+// (tools/mapping_ab.py, config-2 generator, 2,000 steps: at 8,192 g1/g4/g8 = 8.75/5.86/6.01 ms,
+// at 12,288 8.95/7.09/9.94, at 16,384 8.97/8.86/11.3, at 24,576 12.8/13.6/15.9)
+constexpr int64_t kG8AutoMaxBatch = IRK_G8_AUTO_MAX;
+constexpr int64_t kG4AutoMaxBatch = IRK_G4_AUTO_MAX;
 constexpr int64_t kFo8AutoMaxBatch = INT64_MAX;  // first-order mode: stage per lane at every measured batch
                                                  // (tools/fo_bench.py: 1 to 65,536 trajectories)
 
@@ -533,17 +543,18 @@ int launch_g1q(irk_ctx *c, const P &prob, EnsArgs &a, char *ws, cudaStream_t st)
                         });
 }
 
-// Stage-per-lane mapping (ensemble_g8.cuh): one launch, one group of 8 lanes per trajectory.
-template <class P>
-int launch_g8(irk_ctx *c, const P &prob, EnsArgs &a, char *ws, cudaStream_t st) {
+// Stage-per-lane mappings (ensemble_g8.cuh): one launch, one group of G lanes per
+// trajectory (G = 8: one stage per lane; G = 4: two).
+template <class P, int G>
+int launch_gs(irk_ctx *c, const P &prob, EnsArgs &a, char *ws, cudaStream_t st) {
     a.nsteps = c->nsteps;
     a.c0 = 0;
     a.csweeps = nullptr;
     a.perm = nullptr;
     a.nslots = c->batch;
-    const int64_t blocks = (c->batch * 8 + irk::G8_THREADS - 1) / irk::G8_THREADS;
-    irk::ens_g8_kernel<P><<<(unsigned)blocks, irk::G8_THREADS, 0, st>>>(a, prob);
-    int rc = cuda_check(c, cudaGetLastError(), "ens_g8 launch");
+    const int64_t blocks = (c->batch * G + irk::G8_THREADS - 1) / irk::G8_THREADS;
+    irk::ens_gs_kernel<P, G><<<(unsigned)blocks, irk::G8_THREADS, 0, st>>>(a, prob);
+    int rc = cuda_check(c, cudaGetLastError(), "ens_gs launch");
     if (rc) return rc;
     advance_n_kernel<<<1, 1, 0, st>>>(reinterpret_cast<int64_t *>(ws), c->nsteps);
     return cuda_check(c, cudaGetLastError(), "advance_n launch");
@@ -563,12 +574,16 @@ bool nbody8_auto(int NB, int64_t batch) {
     }
 }
 
-// IRK_OPT_MAPPING auto for the per-thread problems: g8 while the batch leaves
-// most g1 lanes of the GPU empty (measured crossover).
-bool use_g8(const irk_ctx *c) {
-    if (c->mapping == IRK_MAP_G8) return true;
-    if (c->mapping == IRK_MAP_G1) return false;
-    return c->batch <= kG8AutoMaxBatch;
+// IRK_OPT_MAPPING auto for the per-thread problems (partitioned mode): lanes per
+// trajectory G = 8 while the batch leaves most g1 lanes of the GPU empty, then
+// G = 4, then one trajectory per lane (measured crossovers).
+int lanes_per_trajectory(const irk_ctx *c) {
+    if (c->mapping == IRK_MAP_G8) return 8;
+    if (c->mapping == IRK_MAP_G4) return 4;
+    if (c->mapping == IRK_MAP_G1) return 1;
+    if (c->batch <= kG8AutoMaxBatch) return 8;
+    if (c->batch <= kG4AutoMaxBatch) return 4;
+    return 1;
 }
 
 // First-order mode (IRK_OPT_MODE = 1; the only mode of non-separable problems):
@@ -606,7 +621,8 @@ int launch_g1(irk_ctx *c, const P &prob, double *y, double t0, char *ws, double 
               int64_t *iters, cudaStream_t st) {
     EnsArgs a = ens_args(c, y, t0, ws, energy, iters);
     const int64_t blocks = (c->batch + irk::G1_THREADS - 1) / irk::G1_THREADS;
-    if (c->mode == 0 && use_g8(c)) return launch_g8(c, prob, a, ws, st);
+    if (c->mode == 0 && lanes_per_trajectory(c) == 8) return launch_gs<P, 8>(c, prob, a, ws, st);
+    if (c->mode == 0 && lanes_per_trajectory(c) == 4) return launch_gs<P, 4>(c, prob, a, ws, st);
     if (c->mode == 0 && c->schedule != 1) return launch_g1q(c, prob, a, ws, st);
     if (c->mode == 1) return launch_first_order(c, prob, y, t0, ws, energy, iters, st);
     return run_chunks(c, a, ws, blocks, irk::G1_THREADS / 32, 32, st, [&](const EnsArgs &aa, int64_t nb) {
@@ -949,8 +965,10 @@ int irk_set_option(irk_ctx *c, int key, int64_t val) {
         c->schedule = (int)val;
         return IRK_OK;
     case IRK_OPT_MAPPING:
-        if (val != IRK_MAP_AUTO && val != IRK_MAP_G1 && val != IRK_MAP_G8)
-            return fail(c, IRK_E_ARG, "irk_set_option: MAPPING must be 0 (auto), 1 (g1) or 8 (g8)");
+        if (val != IRK_MAP_AUTO && val != IRK_MAP_G1 && val != IRK_MAP_G4 && val != IRK_MAP_G8)
+            return fail(c, IRK_E_ARG, "irk_set_option: MAPPING must be 0 (auto), 1 (g1), 4 (g4) or 8 (g8)");
+        if (val == IRK_MAP_G4 && c->problem != IRK_KEPLER && c->problem != IRK_HENON_HEILES)
+            return fail(c, IRK_E_ARG, "irk_set_option: the g4 mapping is built for Kepler and Henon-Heiles");
         if (val == IRK_MAP_G8 && c->problem != IRK_KEPLER && c->problem != IRK_HENON_HEILES && c->problem != IRK_NBODY &&
             c->problem != IRK_SCHWARZSCHILD)
             return fail(c, IRK_E_ARG, "irk_set_option: the g8 mapping is built for Kepler, Henon-Heiles, N-body");

@@ -309,11 +309,13 @@ def test_work_queue_chain_bitwise(irk, orc):
     assert np.array_equal(outs[1][2][idx], orr["iters"]) and np.array_equal(outs[1][4][idx], orr["dhloc"])
 
 
+@pytest.mark.parametrize("G", [8, 4])
 @pytest.mark.parametrize("which", ["kepler", "hh"])
-def test_g8_stage_per_lane_mapping(irk, orc, which):
-    """IRK_OPT_MAPPING = 8 (one stage per lane, warp-shuffle contractions and
-    Delta reduction): bitwise equal to the oracle and to g1 -- states, sweeps,
-    energy samples, Delta H^loc, a diverging trajectory, and two chained calls."""
+def test_g8_stage_per_lane_mapping(irk, orc, which, G):
+    """IRK_OPT_MAPPING = 8 / 4 (G lanes per trajectory, 8/G stages per lane,
+    shared-memory all-gather, xor-shuffle Delta reduction): bitwise equal to the
+    oracle and to g1 -- states, sweeps, energy samples, Delta H^loc, a diverging
+    trajectory, and two chained calls."""
     if which == "kepler":
         w = wl.kepler_ensemble(batch=203, nsteps=600)
         y = w.y.copy()
@@ -322,7 +324,7 @@ def test_g8_stage_per_lane_mapping(irk, orc, which):
         w = wl.henon_heiles(batch=77, nsteps=600)
         y = w.y.copy()
     outs = []
-    for mp in (8, 1):
+    for mp in (G, 1):
         with irk.Integrator(w.problem, w.dim, w.h, w.nsteps // 2, w.batch, w.params, energy_every=50,
                             mapping=mp, local_energy=True) as ig:
             Y = torch.tensor(y, dtype=torch.float64, device="cuda")
