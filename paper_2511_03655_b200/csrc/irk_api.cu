@@ -663,7 +663,21 @@ int launch_chain_t(irk_ctx *c, double *y, double t0, char *ws, double *energy, i
     constexpr int CPB = irk::CH_THREADS / 32;
     const int64_t blocks = (c->batch + CPB - 1) / CPB;
     const double beta = c->params[0];
-    if (c->schedule != 1)
+    // Auto: the work queue, except for batches between one and two resident waves
+    // of warps, where its step-chunk units leave the SMs unevenly loaded (one warp
+    // per chain, chains handed between warps): config 4, 20,000 steps, at 1,536 /
+    // 2,048 chains 212 / 221 ms queued vs 146 / 191 ms chunked, at 3,072 245 vs 281.
+    bool queue = c->schedule != 1;
+    if (c->schedule == 0 && c->balance < 0) {
+        int &bps = c->chain_blocks_per_sm[SPL];
+        if (!bps) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, irk::ens_chain_q_kernel<SPL>, irk::CH_THREADS, 0);
+        int dev = 0, sms = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        const int64_t resident = (int64_t)sms * (bps > 0 ? bps : 1) * CPB;
+        if (c->batch > resident && c->batch <= 2 * resident) queue = false;
+    }
+    if (queue)
         return launch_queue(c, irk::ens_chain_q_kernel<SPL>, irk::CH_THREADS, CPB, &c->chain_blocks_per_sm[SPL], a, ws,
                             st, [&](const EnsArgs &aa, const irk::QueueArgs &qa, unsigned nb) {
                                 irk::ens_chain_q_kernel<SPL><<<nb, irk::CH_THREADS, 0, st>>>(aa, qa, beta);
