@@ -67,8 +67,8 @@ enum irk_option {
     IRK_OPT_MAX_ITERS = 2,    /* sweeps cap per step, default 100 (flagged, step accepted)   */
     IRK_OPT_ENERGY_EVERY = 3, /* E > 0: sample H(y_n) at local steps 0, E, 2E, ... (default 0) */
     IRK_OPT_MAPPING = 4,      /* Kepler / Henon-Heiles (partitioned mode): IRK_MAP_AUTO (default),
-                                 IRK_MAP_G1 = one trajectory per thread, IRK_MAP_G4 = 4 lanes per
-                                 trajectory (two stages per lane), IRK_MAP_G8 = 8 lanes per
+                                 IRK_MAP_G1 = one trajectory per thread, IRK_MAP_G2 / IRK_MAP_G4 =
+                                 2 / 4 lanes per trajectory (4 / 2 stages per lane), IRK_MAP_G8 = 8 lanes per
                                  trajectory, one stage per lane (warp-shuffle contractions and
                                  convergence reduction).  IRK_NBODY: IRK_MAP_G1 = body per lane,
                                  IRK_MAP_G8 = stage per lane (shared-memory all-gather).  Auto
@@ -102,7 +102,7 @@ enum irk_option {
                                  irk_local_energy_error (ensemble problems only)                   */
 };
 
-enum irk_mapping { IRK_MAP_AUTO = 0, IRK_MAP_G1 = 1, IRK_MAP_G4 = 4, IRK_MAP_G8 = 8 };
+enum irk_mapping { IRK_MAP_AUTO = 0, IRK_MAP_G1 = 1, IRK_MAP_G2 = 2, IRK_MAP_G4 = 4, IRK_MAP_G8 = 8 };
 
 /* Create a context for `batch` independent trajectories of `problem` in
  * dimension `dim`, step h (finite, != 0; negative allowed), nsteps >= 0 steps per

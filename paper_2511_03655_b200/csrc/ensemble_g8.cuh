@@ -44,7 +44,7 @@ constexpr int G8_THREADS = 64;  // 8 trajectories per block
 template <class P, int G>
 __global__ void __maxnreg__(G8_MAXREG) ens_gs_kernel(const __grid_constant__ EnsArgs a,
                                                      const __grid_constant__ P prob) {
-    static_assert(G == 8 || G == 4, "G lanes per trajectory: 8 or 4");
+    static_assert(G == 8 || G == 4 || G == 2, "G lanes per trajectory: 8, 4 or 2");
     constexpr int d = P::d, D = 2 * d, SPL = 8 / G, GPB = G8_THREADS / G;
     const unsigned FULL = 0xffffffffu;
     const int64_t B = a.batch;

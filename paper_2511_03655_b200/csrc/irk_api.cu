@@ -76,11 +76,16 @@ constexpr size_t kHeader = 64;
 #ifndef IRK_G4_AUTO_MAX
 #define IRK_G4_AUTO_MAX 16384
 #endif
-// IRK_OPT_MAPPING auto (Kepler, HH): g8 up to kG8AutoMaxBatch, then g4 up to kG4AutoMaxBatch, then g1
-// (tools/mapping_ab.py, config-2 generator, 2,000 steps: at 8,192 g1/g4/g8 = 8.75/5.86/6.01 ms,
-// at 12,288 8.95/7.09/9.94, at 16,384 8.97/8.86/11.3, at 24,576 12.8/13.6/15.9)
+#ifndef IRK_G2_AUTO_MAX
+#define IRK_G2_AUTO_MAX 24576
+#endif
+// IRK_OPT_MAPPING auto (Kepler, HH): g8 up to kG8AutoMaxBatch, g4 up to kG4AutoMaxBatch, g2 up to
+// kG2AutoMaxBatch, then g1 (tools/mapping_ab.py, config-2 generator, 2,000 steps, g1/g2/g4/g8 ms:
+// 8,192: 8.73/7.35/5.87/6.01; 12,288: 8.92/8.89/7.09/9.92; 16,384: 8.94/9.11/8.86/11.3;
+// 24,576: 12.7/11.95/13.6/15.9; 32,768: 12.8/15.1/16.4/20.9)
 constexpr int64_t kG8AutoMaxBatch = IRK_G8_AUTO_MAX;
 constexpr int64_t kG4AutoMaxBatch = IRK_G4_AUTO_MAX;
+constexpr int64_t kG2AutoMaxBatch = IRK_G2_AUTO_MAX;
 constexpr int64_t kFo8AutoMaxBatch = INT64_MAX;  // first-order mode: stage per lane at every measured batch
                                                  // (tools/fo_bench.py: 1 to 65,536 trajectories)
 
@@ -580,9 +585,11 @@ bool nbody8_auto(int NB, int64_t batch) {
 int lanes_per_trajectory(const irk_ctx *c) {
     if (c->mapping == IRK_MAP_G8) return 8;
     if (c->mapping == IRK_MAP_G4) return 4;
+    if (c->mapping == IRK_MAP_G2) return 2;
     if (c->mapping == IRK_MAP_G1) return 1;
     if (c->batch <= kG8AutoMaxBatch) return 8;
     if (c->batch <= kG4AutoMaxBatch) return 4;
+    if (c->batch > kG4AutoMaxBatch * 5 / 4 && c->batch <= kG2AutoMaxBatch) return 2;  // g1 ~ g4 in between
     return 1;
 }
 
@@ -623,6 +630,7 @@ int launch_g1(irk_ctx *c, const P &prob, double *y, double t0, char *ws, double 
     const int64_t blocks = (c->batch + irk::G1_THREADS - 1) / irk::G1_THREADS;
     if (c->mode == 0 && lanes_per_trajectory(c) == 8) return launch_gs<P, 8>(c, prob, a, ws, st);
     if (c->mode == 0 && lanes_per_trajectory(c) == 4) return launch_gs<P, 4>(c, prob, a, ws, st);
+    if (c->mode == 0 && lanes_per_trajectory(c) == 2) return launch_gs<P, 2>(c, prob, a, ws, st);
     if (c->mode == 0 && c->schedule != 1) return launch_g1q(c, prob, a, ws, st);
     if (c->mode == 1) return launch_first_order(c, prob, y, t0, ws, energy, iters, st);
     return run_chunks(c, a, ws, blocks, irk::G1_THREADS / 32, 32, st, [&](const EnsArgs &aa, int64_t nb) {
@@ -979,10 +987,10 @@ int irk_set_option(irk_ctx *c, int key, int64_t val) {
         c->schedule = (int)val;
         return IRK_OK;
     case IRK_OPT_MAPPING:
-        if (val != IRK_MAP_AUTO && val != IRK_MAP_G1 && val != IRK_MAP_G4 && val != IRK_MAP_G8)
-            return fail(c, IRK_E_ARG, "irk_set_option: MAPPING must be 0 (auto), 1 (g1), 4 (g4) or 8 (g8)");
-        if (val == IRK_MAP_G4 && c->problem != IRK_KEPLER && c->problem != IRK_HENON_HEILES)
-            return fail(c, IRK_E_ARG, "irk_set_option: the g4 mapping is built for Kepler and Henon-Heiles");
+        if (val != IRK_MAP_AUTO && val != IRK_MAP_G1 && val != IRK_MAP_G2 && val != IRK_MAP_G4 && val != IRK_MAP_G8)
+            return fail(c, IRK_E_ARG, "irk_set_option: MAPPING must be 0 (auto), 1 (g1), 2 (g2), 4 (g4) or 8 (g8)");
+        if ((val == IRK_MAP_G4 || val == IRK_MAP_G2) && c->problem != IRK_KEPLER && c->problem != IRK_HENON_HEILES)
+            return fail(c, IRK_E_ARG, "irk_set_option: the g2 / g4 mappings are built for Kepler and Henon-Heiles");
         if (val == IRK_MAP_G8 && c->problem != IRK_KEPLER && c->problem != IRK_HENON_HEILES && c->problem != IRK_NBODY &&
             c->problem != IRK_SCHWARZSCHILD)
             return fail(c, IRK_E_ARG, "irk_set_option: the g8 mapping is built for Kepler, Henon-Heiles, N-body");

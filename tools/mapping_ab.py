@@ -1,4 +1,4 @@
-"""g1 vs g4 vs g8 mapping (IRK_OPT_MAPPING) across batch sizes on the config-2
+"""g1 vs g2 vs g4 vs g8 mapping (IRK_OPT_MAPPING) across batch sizes on the config-2
 generator: time per call (CUDA events, best of 3 after a warm-up) and bitwise
 agreement of the mappings.  python tools/mapping_ab.py [nsteps] [lib...]"""
 import json
@@ -17,7 +17,7 @@ res = []
 for B in (512, 2048, 4096, 8192, 12288, 16384, 24576, 32768, 65536):
     w = wl.kepler_ensemble(batch=B, nsteps={nsteps})
     outs, ms = [], []
-    for mp in (1, 4, 8):
+    for mp in (1, 2, 4, 8):
         with irk.Integrator(w.problem, w.dim, w.h, w.nsteps, w.batch, w.params, mapping=mp) as ig:
             y0 = torch.tensor(w.y, dtype=torch.float64, device="cuda"); Y = torch.empty_like(y0)
             ws = ig.new_workspace(); it = torch.zeros(B, dtype=torch.int64, device="cuda")
@@ -30,7 +30,7 @@ for B in (512, 2048, 4096, 8192, 12288, 16384, 24576, 32768, 65536):
             outs.append((Y.cpu(), it.cpu())); ms.append(min(ts[1:]))
     same = all(bool(torch.equal(outs[0][0], o[0]) and torch.equal(outs[0][1], o[1])) for o in outs[1:])
     print(json.dumps({{"lib": os.environ.get("IRK_LIB_OVERRIDE", "default")[-24:], "batch": B, "nsteps": {nsteps},
-                      "g1_ms": ms[0], "g4_ms": ms[1], "g8_ms": ms[2], "bitwise": same}}), flush=True)
+                      "g1_ms": ms[0], "g2_ms": ms[1], "g4_ms": ms[2], "g8_ms": ms[3], "bitwise": same}}), flush=True)
 """
 for lib in LIBS:
     env = dict(os.environ)
