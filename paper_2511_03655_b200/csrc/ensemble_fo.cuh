@@ -27,6 +27,9 @@
 namespace irk {
 
 constexpr int FO_THREADS = 64;
+#ifndef FO8_MAXREG
+#define FO8_MAXREG 168  // ens_fo8: 162 registers, no spills (Schwarzschild, 1,000 steps, B = 1 / 4,096 / 65,536: 2.13 / 3.30 / 38.5 ms; at 128: spills, 2.8 / 3.87 / 39.4)
+#endif
 #ifndef FO_MAXREG
 #define FO_MAXREG 168
 #endif
@@ -250,7 +253,7 @@ namespace irk {
 constexpr int FO8_THREADS = 64;
 
 template <class P>
-__global__ void __maxnreg__(128) ens_fo8_kernel(const __grid_constant__ EnsArgs a, const __grid_constant__ P prob) {
+__global__ void __maxnreg__(FO8_MAXREG) ens_fo8_kernel(const __grid_constant__ EnsArgs a, const __grid_constant__ P prob) {
     constexpr int d = P::d, D = 2 * d;
     const unsigned FULL = 0xffffffffu;
     const int64_t B = a.batch;

@@ -34,7 +34,7 @@ constexpr int G8_THREADS = 64;  // 8 trajectories per block
 #define G8_SMEM 1  // all-gathers through a shared-memory tile (0: shuffles; 2,000 steps at B = 512: 3.65 vs 4.65 ms)
 #endif
 #ifndef G8_MAXREG
-#define G8_MAXREG 128  // config-2 generator, 2,000 steps, B = 2048: 80 regs 5.8 ms, 96: 5.2, 128: 4.7 (g1: 8.7)
+#define G8_MAXREG 168  // g8 uses 119 (B = 2048: 80 regs 5.8 ms, 96: 5.2, 119: 3.7); g4 / g2 use 124 / 156 (at 128 g2 spilled: 7.35 vs 6.88 ms at 8,192)
 #endif
 
 // G lanes per trajectory (G = 8: "g8", one stage per lane; G = 4: "g4", two
