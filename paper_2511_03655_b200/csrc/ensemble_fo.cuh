@@ -320,7 +320,7 @@ __global__ void __maxnreg__(FO8_MAXREG) ens_fo8_kernel(const __grid_constant__ E
         {
             bool ok = true;
             fo_rhs<P, false>(prob, Ys, Ls, ts, ok);
-            if (!ok) fo_rhs<P, true>(prob, Ys, Ls, ts, ok);  // exact intrinsics, same bits
+            if (!ok && live) fo_rhs<P, true>(prob, Ys, Ls, ts, ok);  // exact intrinsics, same bits (live groups)
         }
 #pragma unroll
         for (int l = 0; l < D; ++l) G[s * D + l] = Ls[l] = dmul(sHB[s], Ls[l]);

@@ -199,7 +199,7 @@ __global__ void __maxnreg__(G8_MAXREG) ens_gs_kernel(const __grid_constant__ Ens
 #pragma unroll
             for (int t = 0; t < SPL; ++t)
                 prob.template accel<false>(Qs[t], Fs[t], dadd(tn1, dmul(sC[st0 + t], a.h)), ok);
-            if (!ok)  // exact slow path, same bits
+            if (!ok && live)  // exact slow path, same bits (live groups only)
 #pragma unroll
                 for (int t = 0; t < SPL; ++t)
                     prob.template accel<true>(Qs[t], Fs[t], dadd(tn1, dmul(sC[st0 + t], a.h)), ok);

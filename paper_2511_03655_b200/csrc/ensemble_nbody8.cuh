@@ -266,7 +266,10 @@ __global__ void __maxnreg__(N8_MAXREG) ens_nbody8_kernel(const __grid_constant__
             double F[d];
             bool ok = true;
             n8_accel<NB, false>(Q, F, P, sm, ok);
-            if (!ok) {  // exact intrinsics, same bits (row s of T is free until the Lv store below)
+            // exact intrinsics, same bits (row s of T is free until the Lv store below);
+            // not for idle groups: their zero tiles fail the fast-path range every sweep
+            // (a lone trajectory ran 3x slower for that)
+            if (!ok && live) {
 #pragma unroll
                 for (int l = 0; l < d; ++l) T[s * DP + l] = Q[l];
                 n8_accel_exact_row<NB>(&T[s * DP], P, sm);
