@@ -134,6 +134,7 @@ __global__ void __maxnreg__(G8_MAXREG) ens_gs_kernel(const __grid_constant__ Ens
         ++k;
         // ---- a2 + a5 ----
         double sLq[d], Qs[SPL][d];  // S(Lq) is formed on the fly (the gathered Lq die here)
+        int64_t delta[d];
         bool stop = (k >= 2);
 #if G8_SMEM
 #pragma unroll
@@ -183,13 +184,7 @@ __global__ void __maxnreg__(G8_MAXREG) ens_gs_kernel(const __grid_constant__ Ens
                 const int64_t o = __shfl_xor_sync(FULL, e, off);
                 e = (o > e) ? o : e;
             }
-            if (k >= 2) {  // reading R2, on the bit patterns as in ens_g1q
-                const int64_t mn = (e < p[l]) ? e : p[l];
-                const bool ok = (e == 0) || (m[l] <= mn);
-                m[l] = (p[l] < m[l]) ? p[l] : m[l];
-                p[l] = e;
-                stop = stop && ok;
-            }
+            delta[l] = e;
         }
         // ---- a3: SPL right-hand sides per lane ----
         const double tn1 = dadd(a.t0, dmul((double)(n0 + n), a.h));
@@ -226,6 +221,19 @@ __global__ void __maxnreg__(G8_MAXREG) ens_gs_kernel(const __grid_constant__ Ens
             for (int j = 0; j < 8; ++j) Lvg[j][l] = __shfl_sync(FULL, Lvs[0][l], base + j);
         }
 #endif
+        // the stop test after the right-hand sides: the RHS does not need it, so the
+        // Delta shuffles and the RHS chains share one basic block and overlap
+        if (k >= 2) {  // reading R2, on the bit patterns as in ens_g1q
+#pragma unroll
+            for (int l = 0; l < d; ++l) {
+                const int64_t e = delta[l];
+                const int64_t mn = (e < p[l]) ? e : p[l];
+                const bool ok = (e == 0) || (m[l] <= mn);
+                m[l] = (p[l] < m[l]) ? p[l] : m[l];
+                p[l] = e;
+                stop = stop && ok;
+            }
+        }
         const bool fin = live && (stop || k >= a.max_iters);
         if (fin) {  // ---- a6: update (replicated in the group), history, samples ----
             bool finite = true;
