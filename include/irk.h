@@ -73,18 +73,18 @@ enum irk_option {
                                  convergence reduction).  IRK_NBODY: IRK_MAP_G1 = body per lane,
                                  IRK_MAP_G8 = stage per lane (shared-memory all-gather).  Auto
                                  picks by problem, N and batch size from measured crossovers
-                                 (the chunked IRK_OPT_SCHEDULE = 1 keeps
+                                 ("ens_gs" and "ens_nbody8"; the chunked IRK_OPT_SCHEDULE = 1 keeps
                                  body per lane).  Bitwise-neutral.  */
     IRK_OPT_BALANCE = 5,      /* ensemble scheduling: -1 = auto (default), 0 = off, C > 0 = run the
                                  call in chunks of C steps, re-sorting trajectories by the cost of
-                                 the previous chunk (bitwise-neutral)  */
+                                 the previous chunk (bitwise-neutral, "ens_g1q") */
     IRK_OPT_VSHARDS = 6,      /* IRK_NBODY_DIRECT only: drive P body shards from this process on one
                                  GPU through the sharded code path (testing the exchange layout)   */
     IRK_OPT_SCHEDULE = 8,     /* ensemble launch: 0 = auto (default), 1 = chunked launches with the
                                  cost sort of BALANCE, 2 = one persistent launch whose lanes pull
                                  (trajectory, step-chunk) units from a work queue (per-thread
                                  problems, partitioned mode; BALANCE = C > 0 sets the unit length).
-                                 Bitwise-neutral                          */
+                                 Bitwise-neutral ("ens_g1q")                   */
     IRK_OPT_DEVICE_LOOP = 9,  /* IRK_NBODY_DIRECT: 1 (default) = the fixed-point sweeps run as a CUDA-graph
                                  conditional WHILE loop on the device (one host sync per energy
                                  sample / call); 0 = host loop, one sync per sweep               */
@@ -149,7 +149,7 @@ int irk_integrate_host(irk_ctx *ctx, double *y_host, double t0, double *energy_h
                        int64_t *iters_host, void *stream);
 
 /* H(y) per trajectory (device in, device out [batch]); Neumaier-compensated,
- * canonical term order. */
+ * canonical term order (oracle/CANON.md "Energies"). */
 int irk_energy(irk_ctx *ctx, const double *y, double *H, void *stream);
 
 /* Synchronises `stream`, reduces the workspace stats: out = {trajectories with

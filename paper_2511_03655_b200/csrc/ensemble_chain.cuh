@@ -8,7 +8,7 @@
 // trajectory, so the sweep loop has no divergence at all; the stop test is a
 // warp vote.
 //
-// Canonical RHS (oracle accel_fpu): bond b
+// Canonical RHS (oracle/CANON.md "Right-hand sides", oracle accel_fpu): bond b
 // (b = 0..N, q_{-1} = q_N = 0 in 0-based sites) has D_b = q_b - q_{b-1} and
 // f_b = fma(beta*(D_b*D_b), D_b, D_b); site s gets a_s = f_{s+1} - f_s.  A bond
 // shared by two lanes is evaluated by both with identical operations.

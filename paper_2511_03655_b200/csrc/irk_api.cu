@@ -581,7 +581,7 @@ bool nbody8_auto(int NB, int64_t batch) {
 
 // IRK_OPT_MAPPING auto for the per-thread problems (partitioned mode): lanes per
 // trajectory G = 8 while the batch leaves most g1 lanes of the GPU empty, then
-// G = 4, then one trajectory per lane (measured crossovers).
+// G = 4, then one trajectory per lane ("ens_gs": measured crossovers).
 int lanes_per_trajectory(const irk_ctx *c) {
     if (c->mapping == IRK_MAP_G8) return 8;
     if (c->mapping == IRK_MAP_G4) return 4;

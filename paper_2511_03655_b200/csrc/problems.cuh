@@ -1,6 +1,6 @@
 // Right-hand-side device functors g(q, t) of q' = v, v' = g(q, t) (Eq. ivp2,
 // P:L253) and their Hamiltonians, for the problems with a per-thread state
-// (d small).  Canonical op sequences: DESIGN.md "Right-hand sides".
+// (d small).  Canonical op sequences: oracle/CANON.md "Right-hand sides".
 #pragma once
 #include "fp64.cuh"
 
