@@ -279,7 +279,7 @@ __global__ void __maxnreg__(CH_MAXREG) ens_chain_kernel(const __grid_constant__ 
 // pulls (chain, step-chunk) units until the queue drains; unit (b, c) waits for
 // progress[b] = c.  Same arithmetic per unit, so bitwise any schedule.
 #ifndef CHQ_MAXREG
-#define CHQ_MAXREG 176  // config 4 at 20,000 steps: 164 regs (unbounded) 371 ms, 174-176 regs 326 ms
+#define CHQ_MAXREG 192  // config 4 at 20,000 steps: 164 regs (unbounded) 371 ms, 158: 382, 174: 326.7, cap 192 (176 used): 324.3
 #endif
 template <int SPL>
 __global__ void __maxnreg__(CHQ_MAXREG) ens_chain_q_kernel(const __grid_constant__ EnsArgs a,
