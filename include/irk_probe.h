@@ -20,8 +20,9 @@ int64_t irk_probe_dfma(double *out, int blocks, int iters, void *stream);
 
 /* Bitwise self-check of the branch-free IEEE division / square root used on the
  * hot path (paper_2511_03655_b200/csrc/fp64.cuh): for i < n writes
- * out[4i..4i+3] = {fast a/b (exact fallback applied), __ddiv_rn(a,b),
- * fast sqrt(b) (fallback applied), __dsqrt_rn(b)}; device pointers.
+ * out[6i..6i+5] = {fast a/b (exact fallback applied), __ddiv_rn(a,b),
+ * fast sqrt(b) (fallback applied), __dsqrt_rn(b), fast 1/b (the G = 1 form,
+ * fallback applied), __ddiv_rn(1,b)}; device pointers.
  * Returns 0, or -1 on bad arguments / launch error. */
 int irk_probe_divsqrt(const double *a, const double *b, double *out, int64_t n, void *stream);
 

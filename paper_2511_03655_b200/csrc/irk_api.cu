@@ -356,7 +356,10 @@ int launch_direct(irk_ctx *c, double *y, double t0, char *ws, double *energy, in
     auto force = [&](cudaStream_t s, const irk::NbdArgs &aa, int j_lo, int j_hi) {
         if (j_hi <= j_lo) return;
         const dim3 g((unsigned)((nloc + irk::NBD_FORCE_THREADS - 1) / irk::NBD_FORCE_THREADS), 8, (unsigned)(j_hi - j_lo));
-        irk::nbd_force_kernel<<<g, irk::NBD_FORCE_THREADS, 0, s>>>(aa, j_lo);
+        if (aa.G == 1.0)  // the reciprocal form of the same correctly rounded division
+            irk::nbd_force_kernel<true><<<g, irk::NBD_FORCE_THREADS, 0, s>>>(aa, j_lo);
+        else
+            irk::nbd_force_kernel<false><<<g, irk::NBD_FORCE_THREADS, 0, s>>>(aa, j_lo);
     };
     // Fused exchange: the j-blocks made only of this rank's bodies need no peer
     // data, so they run before the arrival wait (overlapping the exchange, SURVEY

@@ -286,18 +286,20 @@ __global__ void nbd_or_kernel(const __grid_constant__ NbdArgs a) {
 #ifndef NBD_FORCE_MINB
 #define NBD_FORCE_MINB 1
 #endif
-template <bool EXACT>
+template <bool EXACT, bool G1>
 __device__ __forceinline__ void nbd_pair(double xj, double yj, double zj, double mj, double qx, double qy, double qz,
                                          double G, double eps2, double &px, double &py, double &pz, bool &ok) {
     const double dx = dsub(xj, qx), dy = dsub(yj, qy), dz = dsub(zj, qz);
     const double r2 = dfma(dz, dz, dfma(dy, dy, dfma(dx, dx, eps2)));
-    const double w = EXACT ? ddiv(G, dmul(r2, dsqrt(r2))) : ddiv_fast(G, dmul(r2, dsqrt_fast(r2, ok)), ok);
+    const double w = EXACT ? ddiv(G, dmul(r2, dsqrt(r2)))
+                           : (G1 ? drcp_fast(dmul(r2, dsqrt_fast(r2, ok)), ok)   // G == 1: same bits
+                                 : ddiv_fast(G, dmul(r2, dsqrt_fast(r2, ok)), ok));
     const double s = dmul(mj, w);
     px = dfma(s, dx, px);
     py = dfma(s, dy, py);
     pz = dfma(s, dz, pz);
 }
-template <bool EXACT>
+template <bool EXACT, bool G1>
 __device__ __forceinline__ void nbd_pairs(const double *sxyz, const double *sm, int n, double qx, double qy, double qz,
                                           double G, double eps2, double &px, double &py, double &pz, bool &ok) {
     const double2 *x2 = reinterpret_cast<const double2 *>(sxyz);
@@ -305,12 +307,12 @@ __device__ __forceinline__ void nbd_pairs(const double *sxyz, const double *sm, 
 #pragma unroll 2
     for (int t2 = 0; t2 < n / 2; ++t2) {  // bodies 2 t2 and 2 t2 + 1
         const double2 a0 = x2[3 * t2], a1 = x2[3 * t2 + 1], a2 = x2[3 * t2 + 2], mm = m2[t2];
-        nbd_pair<EXACT>(a0.x, a0.y, a1.x, mm.x, qx, qy, qz, G, eps2, px, py, pz, ok);
-        nbd_pair<EXACT>(a1.y, a2.x, a2.y, mm.y, qx, qy, qz, G, eps2, px, py, pz, ok);
+        nbd_pair<EXACT, G1>(a0.x, a0.y, a1.x, mm.x, qx, qy, qz, G, eps2, px, py, pz, ok);
+        nbd_pair<EXACT, G1>(a1.y, a2.x, a2.y, mm.y, qx, qy, qz, G, eps2, px, py, pz, ok);
     }
     if (n & 1) {
         const int t = n - 1;
-        nbd_pair<EXACT>(sxyz[3 * t], sxyz[3 * t + 1], sxyz[3 * t + 2], sm[t], qx, qy, qz, G, eps2, px, py, pz, ok);
+        nbd_pair<EXACT, G1>(sxyz[3 * t], sxyz[3 * t + 1], sxyz[3 * t + 2], sm[t], qx, qy, qz, G, eps2, px, py, pz, ok);
     }
 }
 
@@ -318,6 +320,7 @@ __device__ __forceinline__ uint32_t smem_u32(const void *p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
 
+template <bool G1>
 __global__ void __launch_bounds__(NBD_FORCE_THREADS, NBD_FORCE_MINB) nbd_force_kernel(const __grid_constant__ NbdArgs a,
                                                                                       int jbase) {
     __shared__ __align__(128) double sxyz[3 * NBD_JBLOCK];
@@ -383,10 +386,10 @@ __global__ void __launch_bounds__(NBD_FORCE_THREADS, NBD_FORCE_MINB) nbd_force_k
     // ---- the block's pair sums (pass 1 only if an operand left the fast-path range) ----
     double px = 0.0, py = 0.0, pz = 0.0;
     bool ok = true;
-    if (act) nbd_pairs<false>(sxyz, smass, nj, qx, qy, qz, a.G, a.eps2, px, py, pz, ok);
+    if (act) nbd_pairs<false, G1>(sxyz, smass, nj, qx, qy, qz, a.G, a.eps2, px, py, pz, ok);
     if (__syncthreads_or(!ok)) {  // exact intrinsics, same bits, for the whole block
         px = py = pz = 0.0;
-        if (act) nbd_pairs<true>(sxyz, smass, nj, qx, qy, qz, a.G, a.eps2, px, py, pz, ok);
+        if (act) nbd_pairs<true, G1>(sxyz, smass, nj, qx, qy, qz, a.G, a.eps2, px, py, pz, ok);
     }
     if (!act) return;
     double *P = a.part + ((int64_t)J * 8 + i) * dl;

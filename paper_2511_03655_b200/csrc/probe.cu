@@ -35,13 +35,16 @@ namespace {
 __global__ void divsqrt_probe_kernel(const double *a, const double *b, double *out, int64_t n) {
     const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (i >= n) return;
-    bool ok_d = true, ok_s = true;
+    bool ok_d = true, ok_s = true, ok_r = true;
     const double qf = irk::ddiv_fast(a[i], b[i], ok_d);
     const double sf = irk::dsqrt_fast(b[i], ok_s);
-    out[4 * i + 0] = ok_d ? qf : irk::ddiv(a[i], b[i]);
-    out[4 * i + 1] = irk::ddiv(a[i], b[i]);
-    out[4 * i + 2] = ok_s ? sf : irk::dsqrt(b[i]);
-    out[4 * i + 3] = irk::dsqrt(b[i]);
+    const double rf = irk::drcp_fast(b[i], ok_r);
+    out[6 * i + 0] = ok_d ? qf : irk::ddiv(a[i], b[i]);
+    out[6 * i + 1] = irk::ddiv(a[i], b[i]);
+    out[6 * i + 2] = ok_s ? sf : irk::dsqrt(b[i]);
+    out[6 * i + 3] = irk::dsqrt(b[i]);
+    out[6 * i + 4] = ok_r ? rf : irk::ddiv(1.0, b[i]);
+    out[6 * i + 5] = irk::ddiv(1.0, b[i]);
 }
 }  // namespace
 

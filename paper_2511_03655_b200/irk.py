@@ -242,10 +242,11 @@ def probe_dfma(out, blocks: int, iters: int, stream) -> int:
 
 
 def probe_divsqrt(a, b, stream=None):
-    """(fast a/b, __ddiv_rn, fast sqrt b, __dsqrt_rn) for device float64 tensors a, b."""
+    """(fast a/b, __ddiv_rn, fast sqrt b, __dsqrt_rn, fast 1/b, __ddiv_rn(1, b)) for
+    device float64 tensors a, b."""
     import torch
     n = a.numel()
-    out = torch.empty((n, 4), dtype=torch.float64, device=a.device)
+    out = torch.empty((n, 6), dtype=torch.float64, device=a.device)
     s = torch.cuda.current_stream(a.device) if stream is None else stream
     if lib().irk_probe_divsqrt(_ptr(a), _ptr(b), _ptr(out), n, ctypes.c_void_p(s.cuda_stream)):
         raise IrkError(E_CUDA, "irk_probe_divsqrt failed")

@@ -194,9 +194,9 @@ def test_integrate_host_end_to_end(irk, orc):
 
 
 def test_fast_div_sqrt_bitwise(irk):
-    """The branch-free div/sqrt of the hot path (fp64.cuh) equal __ddiv_rn /
-    __dsqrt_rn bit for bit: 2^26 random operands over many binades, plus
-    specials (0, denormals, inf, nan, negative)."""
+    """The branch-free div/sqrt/reciprocal of the hot path (fp64.cuh) equal
+    __ddiv_rn / __dsqrt_rn / __ddiv_rn(1, .) bit for bit: 2^26 random operands
+    over many binades, plus specials (0, denormals, inf, nan, negative)."""
     g = torch.Generator(device="cuda").manual_seed(1234)
     n = 1 << 24
     for _ in range(4):
@@ -208,6 +208,7 @@ def test_fast_div_sqrt_bitwise(irk):
         out = irk.probe_divsqrt(a, b)
         assert torch.equal(out[:, 0].view(torch.int64), out[:, 1].view(torch.int64))
         assert torch.equal(out[:, 2].view(torch.int64), out[:, 3].view(torch.int64))
+        assert torch.equal(out[:, 4].view(torch.int64), out[:, 5].view(torch.int64))
     sp = torch.tensor([0.0, -0.0, 5e-324, 1e-310, 2.2250738585072014e-308, 1e308, 1.7976931348623157e308,
                        float("inf"), float("-inf"), float("nan"), -1.0, 1.0, 3.0, 1e-300, 4e-320],
                       dtype=torch.float64, device="cuda")
@@ -216,6 +217,7 @@ def test_fast_div_sqrt_bitwise(irk):
     out = irk.probe_divsqrt(A, B).cpu().numpy()
     np.testing.assert_array_equal(out[:, 0].view(np.int64), out[:, 1].view(np.int64))
     np.testing.assert_array_equal(out[:, 2].view(np.int64), out[:, 3].view(np.int64))
+    np.testing.assert_array_equal(out[:, 4].view(np.int64), out[:, 5].view(np.int64))
 
 
 def test_cost_balanced_schedule_is_bitwise_neutral(irk, orc):
