@@ -290,7 +290,7 @@ def run_ours(args):
                          "traffic_unit": "DRAM bytes per ens_g1q launch (ncu --set full, profiles/r1)",
                          "peak_note": f"FP64 pipe: {SM_COUNT} SM x {FP64_FMA_PER_CLK_PER_SM} FMA/clk x 2 x {sm_max:.0f} MHz; "
                                       f"DFMA probe measured {probe:.2f} TFLOP/s on this GPU",
-                         "kernel": "ens_g1q_kernel<Kepler>",
+                         "kernel": "ens_g1q_kernel<KeplerT<true>> (GM = 1: reciprocal form of the division)",
                          "timed": "CUDA events around irk_integrate: 1 ens_g1q launch (+2 memsets, advance_n)", "flops_per_launch": fl,
                          "sweeps_per_step": sweeps / (B * w.nsteps)},
             "e2e": {"value": world * B * w.nsteps * args.steps / Te, "unit": UNIT,

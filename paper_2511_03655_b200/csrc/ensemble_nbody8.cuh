@@ -40,7 +40,7 @@ constexpr int N8_THREADS = 64;  // 8 groups (trajectories) per block
 // NB in cyclic order, d = Q_j - Q_i, a_i = fma(m_j w_ij, d, a_i)  (oracle
 // accel_nbody_pairs; w_ij = w_ji bit for bit since the squared differences are
 // the same).
-template <int NB, bool EXACT>
+template <int NB, bool EXACT, bool G1 = false>
 __device__ __forceinline__ void n8_accel(const double *Q, double *A, const NBodyParams &P, const double *sm,
                                          bool &ok) {
     constexpr int NP = NB * (NB - 1) / 2;
@@ -57,7 +57,9 @@ __device__ __forceinline__ void n8_accel(const double *Q, double *A, const NBody
             const double dx = dsub(Q[3 * j], Q[3 * i]), dy = dsub(Q[3 * j + 1], Q[3 * i + 1]),
                          dz = dsub(Q[3 * j + 2], Q[3 * i + 2]);
             const double r2 = dfma(dz, dz, dfma(dy, dy, dfma(dx, dx, P.eps2)));
-            w[p] = EXACT ? ddiv(P.G, dmul(r2, dsqrt(r2))) : ddiv_fast(P.G, dmul(r2, dsqrt_fast(r2, ok)), ok);
+            w[p] = EXACT ? ddiv(P.G, dmul(r2, dsqrt(r2)))
+                         : (G1 ? drcp_fast(dmul(r2, dsqrt_fast(r2, ok)), ok)  // G == 1: same bits
+                               : ddiv_fast(P.G, dmul(r2, dsqrt_fast(r2, ok)), ok));
         }
 #pragma unroll
     for (int i = 0; i < NB; ++i) {
@@ -94,7 +96,7 @@ __device__ __noinline__ void n8_accel_exact_row(double *row, const NBodyParams &
     for (int l = 0; l < d; ++l) row[l] = F[l];
 }
 
-template <int NB>
+template <int NB, bool G1>
 __global__ void __maxnreg__(N8_MAXREG) ens_nbody8_kernel(const __grid_constant__ EnsArgs a,
                                                         const __grid_constant__ QueueArgs qa,
                                                         const __grid_constant__ NBodyParams P) {
@@ -265,7 +267,7 @@ __global__ void __maxnreg__(N8_MAXREG) ens_nbody8_kernel(const __grid_constant__
         {
             double F[d];
             bool ok = true;
-            n8_accel<NB, false>(Q, F, P, sm, ok);
+            n8_accel<NB, false, G1>(Q, F, P, sm, ok);
             // exact intrinsics, same bits (row s of T is free until the Lv store below);
             // not for idle groups: their zero tiles fail the fast-path range every sweep
             // (a lone trajectory ran 3x slower for that)

@@ -70,6 +70,9 @@ struct irk_ctx {
 namespace {
 
 constexpr size_t kHeader = 64;
+#ifndef IRK_UNIT_G
+#define IRK_UNIT_G 1  // G = 1 / GM = 1 kernels use the reciprocal form of the division (fp64.cuh drcp_fast)
+#endif
 #ifndef IRK_G8_AUTO_MAX
 #define IRK_G8_AUTO_MAX 6144
 #endif
@@ -356,7 +359,7 @@ int launch_direct(irk_ctx *c, double *y, double t0, char *ws, double *energy, in
     auto force = [&](cudaStream_t s, const irk::NbdArgs &aa, int j_lo, int j_hi) {
         if (j_hi <= j_lo) return;
         const dim3 g((unsigned)((nloc + irk::NBD_FORCE_THREADS - 1) / irk::NBD_FORCE_THREADS), 8, (unsigned)(j_hi - j_lo));
-        if (aa.G == 1.0)  // the reciprocal form of the same correctly rounded division
+        if (IRK_UNIT_G && aa.G == 1.0)  // the reciprocal form of the same correctly rounded division
             irk::nbd_force_kernel<true><<<g, irk::NBD_FORCE_THREADS, 0, s>>>(aa, j_lo);
         else
             irk::nbd_force_kernel<false><<<g, irk::NBD_FORCE_THREADS, 0, s>>>(aa, j_lo);
@@ -653,11 +656,17 @@ int launch_nbody_t(irk_ctx *c, double *y, double t0, char *ws, double *energy, i
     // stage-per-lane (ensemble_nbody8.cuh) when asked or where auto measured it faster; the
     // chunked schedule (IRK_OPT_SCHEDULE = 1) keeps body-per-lane
     if (c->mapping == IRK_MAP_G8 || (c->mapping == IRK_MAP_AUTO && c->schedule != 1 && nbody8_auto(NB, c->batch)))
-        return launch_queue(c, irk::ens_nbody8_kernel<NB>, irk::N8_THREADS, irk::N8_THREADS / 8,
-                            &c->nbody8_blocks_per_sm[NB], a, ws, st,
-                            [&](const EnsArgs &aa, const irk::QueueArgs &qa, unsigned nb) {
-                                irk::ens_nbody8_kernel<NB><<<nb, irk::N8_THREADS, 0, st>>>(aa, qa, P);
-                            });
+        return (IRK_UNIT_G && P.G == 1.0)
+                   ? launch_queue(c, irk::ens_nbody8_kernel<NB, true>, irk::N8_THREADS, irk::N8_THREADS / 8,
+                                  &c->nbody8_blocks_per_sm[NB], a, ws, st,
+                                  [&](const EnsArgs &aa, const irk::QueueArgs &qa, unsigned nb) {
+                                      irk::ens_nbody8_kernel<NB, true><<<nb, irk::N8_THREADS, 0, st>>>(aa, qa, P);
+                                  })
+                   : launch_queue(c, irk::ens_nbody8_kernel<NB, false>, irk::N8_THREADS, irk::N8_THREADS / 8,
+                                  &c->nbody8_blocks_per_sm[NB], a, ws, st,
+                                  [&](const EnsArgs &aa, const irk::QueueArgs &qa, unsigned nb) {
+                                      irk::ens_nbody8_kernel<NB, false><<<nb, irk::N8_THREADS, 0, st>>>(aa, qa, P);
+                                  });
     if (c->schedule != 1)
         return launch_queue(c, irk::ens_nbody_q_kernel<NB>, irk::NB_THREADS, GPW * WPB, &c->nbody_blocks_per_sm[NB], a,
                             ws, st, [&](const EnsArgs &aa, const irk::QueueArgs &qa, unsigned nb) {
@@ -1039,8 +1048,13 @@ int irk_integrate(irk_ctx *c, double *y, double t0, void *workspace, double *ene
     if (rc) return rc;
     switch (c->problem) {
     case IRK_KEPLER: {
-        irk::Kepler P{c->params[0]};
-        rc = launch_g1(c, P, y, t0, ws, energy, iters, st);
+        if (IRK_UNIT_G && c->params[0] == 1.0) {  // GM = 1: the reciprocal form of the same division
+            irk::KeplerG1 P{c->params[0]};
+            rc = launch_g1(c, P, y, t0, ws, energy, iters, st);
+        } else {
+            irk::Kepler P{c->params[0]};
+            rc = launch_g1(c, P, y, t0, ws, energy, iters, st);
+        }
         break;
     }
     case IRK_HENON_HEILES: {

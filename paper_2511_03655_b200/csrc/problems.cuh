@@ -7,7 +7,10 @@
 namespace irk {
 
 // Planar Kepler, H = |v|^2/2 - GM/|q| (the 2-body reduction of Eq. Ham2).
-struct Kepler {
+// UNIT_GM: GM == 1 (every Kepler workload here), the division in its reciprocal
+// form (drcp_fast, same bits); chosen at launch from the parameter.
+template <bool UNIT_GM>
+struct KeplerT {
     static constexpr int d = 2;
     static constexpr bool first_order = false;  // g(q, t) of q'' = g: (v, g) in first-order mode
     double GM;
@@ -17,7 +20,7 @@ struct Kepler {
     __device__ __forceinline__ void accel(const double *q, double *a, double /*t*/, bool &ok) const {
         double r2 = dfma(q[0], q[0], dmul(q[1], q[1]));
         double r3 = dmul(r2, EXACT ? dsqrt(r2) : dsqrt_fast(r2, ok));
-        double w = EXACT ? ddiv(GM, r3) : ddiv_fast(GM, r3, ok);
+        double w = EXACT ? ddiv(GM, r3) : (UNIT_GM ? drcp_fast(r3, ok) : ddiv_fast(GM, r3, ok));
         a[0] = -dmul(w, q[0]);
         a[1] = -dmul(w, q[1]);
     }
@@ -29,6 +32,8 @@ struct Kepler {
         return n.result();
     }
 };
+using Kepler = KeplerT<false>;
+using KeplerG1 = KeplerT<true>;
 
 // Canonical sine and cosine (oracle/CANON.md "Canonical sin / cos"): x = k pi/2 + t
 // by a three-part Cody-Waite reduction, Taylor polynomials of degree 19 / 20 in
