@@ -41,7 +41,10 @@
 namespace irk {
 
 constexpr int NBD_JBLOCK = 1024;  // canonical j-block (oracle NB_BLOCK)
-constexpr int NBD_FORCE_THREADS = 128;
+#ifndef NBD_FORCE_BLOCK
+#define NBD_FORCE_BLOCK 256  // config 5, 100 steps: 64 threads 531 ms, 128: 524, 256: 519 (the j-block fill amortised over more bodies)
+#endif
+constexpr int NBD_FORCE_THREADS = NBD_FORCE_BLOCK;
 
 struct NbdCtl {           // device-side control block (one per process)
     int64_t n;            // steps completed in this call
