@@ -96,7 +96,10 @@ enum irk_option {
                                  ranks in one NVLink domain) and its last CTA signals arrival; the
                                  next kernel waits for all ranks (IRK_E_COMM after 60 s).  The window
                                  is created collectively on the first fused irk_integrate and freed
-                                 by irk_destroy.  Bitwise-neutral            */
+                                 by irk_destroy.  Bitwise-neutral.  With more
+                                 than one rank this mode has not run across GPUs yet: irk_integrate
+                                 returns IRK_E_STATE unless the environment sets
+                                 IRK_EXPERIMENTAL_FUSED_EXCHANGE=1                                  */
     IRK_OPT_LOCAL_ENERGY = 7  /* 1: track Delta H^loc_max = max_n |(H(y_n)-H(y_{n-1}))/H(y_{n-1})|
                                  (Eq. DHlocmax) over each call, in-kernel; read it with
                                  irk_local_energy_error (ensemble problems only)                   */
@@ -119,8 +122,12 @@ int irk_set_option(irk_ctx *ctx, int key, int64_t val);
 
 /* Read an option (any IRK_OPT_*) or a read-only fact about the last call:
  * IRK_INFO_DEVICE_LOOP_USED = 1 if the last IRK_NBODY_DIRECT call ran its sweeps as
- * the device-side graph loop (0: host loop).  IRK_E_ARG for an unknown key. */
-enum irk_info { IRK_INFO_DEVICE_LOOP_USED = 100 };
+ * the device-side graph loop (0: host loop); IRK_INFO_MAPPING_USED = the IRK_MAP_*
+ * value IRK_OPT_MAPPING (auto included) resolved to in the last irk_integrate
+ * (IRK_MAP_G1/G2/G4/G8 for Kepler, Henon-Heiles, Schwarzschild; G1 = body per lane,
+ * G8 = stage per lane for IRK_NBODY; 0 for IRK_FPU_BETA and IRK_NBODY_DIRECT, which
+ * have one mapping).  IRK_E_ARG for an unknown key. */
+enum irk_info { IRK_INFO_DEVICE_LOOP_USED = 100, IRK_INFO_MAPPING_USED = 101 };
 int irk_get_option(const irk_ctx *ctx, int key, int64_t *val);
 
 /* Bytes of caller-owned DEVICE workspace irk_integrate needs.  Layout: a

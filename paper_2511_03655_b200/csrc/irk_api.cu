@@ -6,10 +6,13 @@
 #include <cstddef>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
 #include <vector>
+
+#include <nvtx3/nvToolsExt.h>  // header-only NVTX v3: ranges for nsys timelines (no-op without a tool)
 
 #include "../../include/irk.h"
 #include "balance.cuh"
@@ -59,6 +62,7 @@ struct irk_ctx {
     int vshards = 1;               // virtual shards on one GPU (IRK_OPT_VSHARDS)
     int device_loop = 1;           // IRK_OPT_DEVICE_LOOP (large-N path)
     int device_loop_used = 0;      // IRK_INFO_DEVICE_LOOP_USED: the last call ran the graph loop
+    int mapping_used = 0;          // IRK_INFO_MAPPING_USED: the IRK_MAP_* the last call resolved to
     void *nccl_comm = nullptr;
     // fused exchange (IRK_OPT_EXCHANGE = 1): symmetric NCCL window [header | 2 x P x stride]
     int exchange = 0;
@@ -107,6 +111,12 @@ int cuda_check(irk_ctx *c, cudaError_t e, const char *what) {
     return fail(c, IRK_E_CUDA, "%s: %s", what, cudaGetErrorString(e));
 }
 
+// NVTX range for the phases of a call (irk_integrate, config-5 segments, exchanges).
+struct NvtxRange {
+    explicit NvtxRange(const char *name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+};
+
 // rows of y / history held by this process (the local bodies' 6N/P rows when sharded under NCCL)
 int64_t local_dim(const irk_ctx *c) {
     return (c->problem == IRK_NBODY_DIRECT && c->nccl_comm) ? c->dim / c->nranks : c->dim;
@@ -126,21 +136,21 @@ int n_params_expected(int problem, int dim) {
     return -1;
 }
 
-// mu~, nu~, c~ into the constant bank of the current device, once per device.
-std::mutex g_const_mu;
-bool g_const_done[64] = {};
-
-int upload_constants(irk_ctx *c) {
-    int dev = 0;
-    int rc = cuda_check(c, cudaGetDevice(&dev), "cudaGetDevice");
-    if (rc) return rc;
-    std::lock_guard<std::mutex> lk(g_const_mu);
-    if (dev < 64 && g_const_done[dev]) return IRK_OK;
-    if ((rc = cuda_check(c, cudaMemcpyToSymbol(irk::c_mu, c->T.mu, sizeof c->T.mu), "upload mu"))) return rc;
-    if ((rc = cuda_check(c, cudaMemcpyToSymbol(irk::c_nu, c->T.nu, sizeof c->T.nu), "upload nu"))) return rc;
-    if ((rc = cuda_check(c, cudaMemcpyToSymbol(irk::c_c, c->T.c, sizeof c->T.c), "upload c"))) return rc;
-    if (dev < 64) g_const_done[dev] = true;
-    return IRK_OK;
+// mu~, nu~, c~ into the constant bank of the current device, enqueued on the
+// call's stream every call (1.1 KB).  The values are the same for every ctx
+// (one fixed tableau), so concurrent calls on other streams read the same bits;
+// uploading per call (not once per device index) survives a cudaDeviceReset,
+// which would otherwise leave the bank zeroed behind a stale "done" flag.
+int upload_constants(irk_ctx *c, cudaStream_t st) {
+    int rc;
+    if ((rc = cuda_check(c, cudaMemcpyToSymbolAsync(irk::c_mu, c->T.mu, sizeof c->T.mu, 0, cudaMemcpyHostToDevice, st),
+                         "upload mu")))
+        return rc;
+    if ((rc = cuda_check(c, cudaMemcpyToSymbolAsync(irk::c_nu, c->T.nu, sizeof c->T.nu, 0, cudaMemcpyHostToDevice, st),
+                         "upload nu")))
+        return rc;
+    return cuda_check(c, cudaMemcpyToSymbolAsync(irk::c_c, c->T.c, sizeof c->T.c, 0, cudaMemcpyHostToDevice, st),
+                      "upload c");
 }
 
 __global__ void advance_n_kernel(int64_t *n_done, int64_t nsteps) { *n_done += nsteps; }
@@ -261,6 +271,15 @@ int launch_direct(irk_ctx *c, double *y, double t0, char *ws, double *energy, in
     int rc;
     if (c->exchange == 1 && !nccl)
         return fail(c, IRK_E_STATE, "irk_integrate: IRK_OPT_EXCHANGE = 1 needs a communicator (irk_set_comm)");
+    // The fused exchange's cross-GPU memory ordering has only run at one rank
+    // (DESIGN.md section 8); more ranks need an explicit opt-in until it has run there.
+    if (fused && c->nranks > 1) {
+        const char *ok = getenv("IRK_EXPERIMENTAL_FUSED_EXCHANGE");
+        if (!ok || strcmp(ok, "1") != 0)
+            return fail(c, IRK_E_STATE, "irk_integrate: IRK_OPT_EXCHANGE = 1 with %d ranks is experimental "
+                                        "(never run across GPUs); set IRK_EXPERIMENTAL_FUSED_EXCHANGE=1 to use it",
+                        c->nranks);
+    }
     if (!c->d_mass) {
         if ((rc = cuda_check(c, cudaMalloc(&c->d_mass, sizeof(double) * N), "cudaMalloc mass"))) return rc;
         if ((rc = cuda_check(c, cudaMallocHost(&c->h_ctl, sizeof(irk::NbdCtl)), "cudaMallocHost ctl"))) return rc;
@@ -328,6 +347,7 @@ int launch_direct(irk_ctx *c, double *y, double t0, char *ws, double *energy, in
     const unsigned cb = (unsigned)((dl + 127) / 128);
     const int64_t E = c->energy_every;
     auto sample = [&](int64_t idx) -> int {
+        NvtxRange range("irk:energy_sample");
         for (int t = 0; t < nlocal; ++t)
             cudaMemcpyAsync(Qall + 3 * A[t].b0, A[t].yq, sizeof(double) * dl, cudaMemcpyDeviceToDevice, st);
         if (nccl) {
@@ -441,6 +461,7 @@ int launch_direct(irk_ctx *c, double *y, double t0, char *ws, double *energy, in
     c->device_loop_used = gexec ? 1 : 0;
     if (gexec) {
         while (n < c->nsteps) {
+            NvtxRange range("irk:device_loop_segment");
             const int64_t target = (E > 0 && energy) ? ((n / E + 1) * E < c->nsteps ? (n / E + 1) * E : c->nsteps)
                                                      : c->nsteps;
             c->h_ctl->target = target;
@@ -461,6 +482,7 @@ int launch_direct(irk_ctx *c, double *y, double t0, char *ws, double *energy, in
         cudaGraphExecDestroy(gexec);
     } else {
         while (n < c->nsteps) {
+            NvtxRange range("irk:host_loop_sweep");
             if ((rc = enqueue_sweep(st, 0, 0))) return rc;
             cudaMemcpyAsync(c->h_ctl, ctl, sizeof(irk::NbdCtl), cudaMemcpyDeviceToHost, st);
             if ((rc = cuda_check(c, cudaStreamSynchronize(st), "direct sweep"))) return rc;
@@ -532,6 +554,10 @@ int launch_queue(irk_ctx *c, KernelPtr kernel, int threads, int spb, int *bps_ca
     if (chunk < 1) chunk = 1;
     qa.qchunk = chunk;
     qa.nchunks = c->nsteps > 0 ? (c->nsteps + chunk - 1) / chunk : 1;
+    // progress[] / orphan[] hold chunk indices + 1 as int32
+    if (qa.nchunks >= INT32_MAX)
+        return fail(c, IRK_E_ARG, "irk_integrate: %lld step chunks per call exceed the work queue's int32 counters "
+                                  "(raise IRK_OPT_BALANCE or split the call)", (long long)qa.nchunks);
     a.nsteps = c->nsteps;
     a.c0 = 0;
     a.csweeps = nullptr;
@@ -605,7 +631,9 @@ template <class P>
 int launch_first_order(irk_ctx *c, const P &prob, double *y, double t0, char *ws, double *energy, int64_t *iters,
                        cudaStream_t st) {
     EnsArgs a = ens_args(c, y, t0, ws, energy, iters);
-    if (c->mapping == IRK_MAP_G8 || (c->mapping == IRK_MAP_AUTO && c->batch <= kFo8AutoMaxBatch)) {
+    const bool fo8 = c->mapping == IRK_MAP_G8 || (c->mapping == IRK_MAP_AUTO && c->batch <= kFo8AutoMaxBatch);
+    c->mapping_used = fo8 ? IRK_MAP_G8 : IRK_MAP_G1;
+    if (fo8) {
         a.nsteps = c->nsteps;  // stage per lane: one launch, one group of 8 lanes per trajectory
         a.c0 = 0;
         a.csweeps = nullptr;
@@ -634,6 +662,7 @@ int launch_g1(irk_ctx *c, const P &prob, double *y, double t0, char *ws, double 
               int64_t *iters, cudaStream_t st) {
     EnsArgs a = ens_args(c, y, t0, ws, energy, iters);
     const int64_t blocks = (c->batch + irk::G1_THREADS - 1) / irk::G1_THREADS;
+    c->mapping_used = c->mode == 0 ? lanes_per_trajectory(c) : IRK_MAP_G1;  // (first-order: set below)
     if (c->mode == 0 && lanes_per_trajectory(c) == 8) return launch_gs<P, 8>(c, prob, a, ws, st);
     if (c->mode == 0 && lanes_per_trajectory(c) == 4) return launch_gs<P, 4>(c, prob, a, ws, st);
     if (c->mode == 0 && lanes_per_trajectory(c) == 2) return launch_gs<P, 2>(c, prob, a, ws, st);
@@ -655,7 +684,10 @@ int launch_nbody_t(irk_ctx *c, double *y, double t0, char *ws, double *energy, i
     const int64_t blocks = (c->batch + GPW * WPB - 1) / (GPW * WPB);
     // stage-per-lane (ensemble_nbody8.cuh) when asked or where auto measured it faster; the
     // chunked schedule (IRK_OPT_SCHEDULE = 1) keeps body-per-lane
-    if (c->mapping == IRK_MAP_G8 || (c->mapping == IRK_MAP_AUTO && c->schedule != 1 && nbody8_auto(NB, c->batch)))
+    const bool stage_per_lane =
+        c->mapping == IRK_MAP_G8 || (c->mapping == IRK_MAP_AUTO && c->schedule != 1 && nbody8_auto(NB, c->batch));
+    c->mapping_used = stage_per_lane ? IRK_MAP_G8 : IRK_MAP_G1;
+    if (stage_per_lane)
         return (IRK_UNIT_G && P.G == 1.0)
                    ? launch_queue(c, irk::ens_nbody8_kernel<NB, true>, irk::N8_THREADS, irk::N8_THREADS / 8,
                                   &c->nbody8_blocks_per_sm[NB], a, ws, st,
@@ -1026,6 +1058,7 @@ int irk_get_option(const irk_ctx *c, int key, int64_t *val) {
     case IRK_OPT_DEVICE_LOOP: *val = c->device_loop; return IRK_OK;
     case IRK_OPT_EXCHANGE: *val = c->exchange; return IRK_OK;
     case IRK_INFO_DEVICE_LOOP_USED: *val = c->device_loop_used; return IRK_OK;
+    case IRK_INFO_MAPPING_USED: *val = c->mapping_used; return IRK_OK;
     }
     return IRK_E_ARG;
 }
@@ -1044,7 +1077,11 @@ int irk_integrate(irk_ctx *c, double *y, double t0, void *workspace, double *ene
     if (c->energy_every > 0 && !energy) return fail(c, IRK_E_ARG, "irk_integrate: ENERGY_EVERY set but energy == NULL");
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
     char *ws = static_cast<char *>(workspace);
-    int rc = upload_constants(c);
+    static const char *kNames[] = {"irk_integrate", "irk_integrate:kepler", "irk_integrate:nbody",
+                                   "irk_integrate:fpu_beta", "irk_integrate:henon_heiles",
+                                   "irk_integrate:nbody_direct", "irk_integrate:schwarzschild"};
+    NvtxRange range(kNames[(c->problem >= 1 && c->problem <= 6) ? c->problem : 0]);
+    int rc = upload_constants(c, st);
     if (rc) return rc;
     switch (c->problem) {
     case IRK_KEPLER: {
@@ -1071,9 +1108,11 @@ int irk_integrate(irk_ctx *c, double *y, double t0, void *workspace, double *ene
         rc = launch_nbody(c, y, t0, ws, energy, iters, st);
         break;
     case IRK_FPU_BETA:
+        c->mapping_used = 0;
         rc = launch_chain(c, y, t0, ws, energy, iters, st);
         break;
     case IRK_NBODY_DIRECT:
+        c->mapping_used = 0;
         rc = launch_direct(c, y, t0, ws, energy, iters, st);
         break;
     default: return fail(c, IRK_E_ARG, "irk_integrate: problem not supported");

@@ -22,6 +22,7 @@ OPT_DEVICE_LOOP = 9
 OPT_EXCHANGE = 10  # IRK_NBODY_DIRECT under set_comm: 0 = ncclAllGather, 1 = fused NVLink stores
 EXCHANGE_ALLGATHER, EXCHANGE_FUSED = 0, 1
 INFO_DEVICE_LOOP_USED = 100
+INFO_MAPPING_USED = 101
 PARTITIONED, FIRST_ORDER = 0, 1
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
@@ -92,6 +93,27 @@ def tableau():
 
 def _ptr(t):
     return None if t is None else ctypes.c_void_p(t.data_ptr())
+
+
+def _need(t, name, dtype, shape=None, device=None, min_numel=None):
+    """Explicit checks of a device buffer before its raw pointer crosses the C ABI
+    (which cannot see sizes): dtype, CUDA, contiguity, shape / size, device.
+    Raises ValueError (not assert: survives python -O)."""
+    import torch
+    if not isinstance(t, torch.Tensor):
+        raise ValueError(f"{name}: expected a torch tensor, got {type(t).__name__}")
+    if t.dtype != dtype:
+        raise ValueError(f"{name}: dtype {t.dtype}, expected {dtype}")
+    if not t.is_cuda:
+        raise ValueError(f"{name}: must be a CUDA tensor")
+    if not t.is_contiguous():
+        raise ValueError(f"{name}: must be contiguous")
+    if device is not None and t.device != device:
+        raise ValueError(f"{name}: on {t.device}, expected {device}")
+    if shape is not None and tuple(t.shape) != tuple(shape):
+        raise ValueError(f"{name}: shape {tuple(t.shape)}, expected {tuple(shape)}")
+    if min_numel is not None and t.numel() < min_numel:
+        raise ValueError(f"{name}: {t.numel()} elements, need >= {min_numel}")
 
 
 class Integrator:
@@ -166,9 +188,16 @@ class Integrator:
     def integrate(self, y, workspace, *, t0: float = 0.0, energy=None, iters=None, stream=None):
         """Advance y in place on the device (irk_integrate); asynchronous on `stream`."""
         import torch
-        assert y.dtype == torch.float64 and y.is_cuda and y.is_contiguous()
-        assert tuple(y.shape) == (self.local_dim, self.batch)
-        assert workspace.numel() >= self.workspace_bytes
+        _need(y, "y", torch.float64, shape=(self.local_dim, self.batch))
+        _need(workspace, "workspace", torch.uint8, device=y.device, min_numel=self.workspace_bytes)
+        if self.energy_every > 0 and energy is None:
+            raise ValueError("energy: required when energy_every > 0")
+        if self.energy_every <= 0:
+            energy = None          # no samples are written
+        if energy is not None:
+            _need(energy, "energy", torch.float64, shape=(self.n_energy(), self.batch), device=y.device)
+        if iters is not None:
+            _need(iters, "iters", torch.int64, shape=(self.batch,), device=y.device)
         s = torch.cuda.current_stream(y.device) if stream is None else stream
         self._check(lib().irk_integrate(self._ctx, _ptr(y), t0, _ptr(workspace), _ptr(energy),
                                         _ptr(iters), ctypes.c_void_p(s.cuda_stream)))
@@ -177,8 +206,9 @@ class Integrator:
                        want_iters=True, stream=None):
         """End-to-end call from host memory (irk_integrate_host); returns (energy, iters)."""
         import torch
-        assert y_host.dtype == np.float64 and y_host.flags.c_contiguous
-        assert y_host.shape == (self.local_dim, self.batch)
+        if not (isinstance(y_host, np.ndarray) and y_host.dtype == np.float64 and y_host.flags.c_contiguous
+                and y_host.shape == (self.local_dim, self.batch)):
+            raise ValueError(f"y_host: need a C-contiguous float64 ndarray of shape {(self.local_dim, self.batch)}")
         E = np.zeros((self.n_energy(), self.batch)) if (want_energy and self.energy_every > 0) else None
         it = np.zeros(self.batch, dtype=np.int64) if want_iters else None
         s = torch.cuda.current_stream() if stream is None else stream
@@ -190,14 +220,17 @@ class Integrator:
 
     def energy(self, y, out=None, stream=None):
         import torch
+        _need(y, "y", torch.float64, shape=(self.local_dim, self.batch))
         if out is None:
             out = torch.empty(self.batch, dtype=torch.float64, device=y.device)
+        _need(out, "out", torch.float64, shape=(self.batch,), device=y.device)
         s = torch.cuda.current_stream(y.device) if stream is None else stream
         self._check(lib().irk_energy(self._ctx, _ptr(y), _ptr(out), ctypes.c_void_p(s.cuda_stream)))
         return out
 
     def stats(self, workspace, stream=None):
         import torch
+        _need(workspace, "workspace", torch.uint8, min_numel=self.workspace_bytes)
         out = np.zeros(4, dtype=np.int64)
         s = torch.cuda.current_stream(workspace.device) if stream is None else stream
         rc = lib().irk_stats(self._ctx, _ptr(workspace), ctypes.c_void_p(s.cuda_stream),
@@ -220,6 +253,7 @@ class Integrator:
     def local_energy_error(self, workspace, stream=None):
         """Per-trajectory Delta H^loc_max of the last call (IRK_OPT_LOCAL_ENERGY)."""
         import torch
+        _need(workspace, "workspace", torch.uint8, min_numel=self.workspace_bytes)
         out = torch.empty(self.batch, dtype=torch.float64, device=workspace.device)
         s = torch.cuda.current_stream(workspace.device) if stream is None else stream
         self._check(lib().irk_local_energy_error(self._ctx, _ptr(workspace), _ptr(out),
