@@ -64,7 +64,7 @@ def build(force: bool = False, verbose: bool = False, out: str | None = None,
     if not force and out is None and not _stale():
         return LIB
     os.makedirs(OUT, exist_ok=True)
-    bdir = os.path.join(OUT, "obj")
+    bdir = os.path.join(OUT, "obj") if out is None else lib_path + ".obj"  # variants build in parallel
     os.makedirs(bdir, exist_ok=True)
     nvcc = _nvcc()
     objs = []

@@ -71,6 +71,33 @@ __device__ __forceinline__ void st_release(int32_t *p, int32_t v) {
     asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
+// Work-unit trace (measurement builds only, -DIRK_TRACE; tools/unit_trace.py):
+// per finished unit {c << 32 | b, smid << 48 | block << 16 | thread, t_fetch, t_start, t_end, sweeps}
+// (globaltimer ns).  Absent from the product build.
+#ifdef IRK_TRACE
+__device__ unsigned long long *g_irk_trace;
+__device__ unsigned long long g_irk_trace_n, g_irk_trace_cap;
+__device__ __forceinline__ unsigned long long irk_now() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+__device__ __forceinline__ void irk_trace_unit(int64_t c, int64_t b, unsigned long long tf, unsigned long long ts,
+                                               int64_t sweeps) {
+    const unsigned long long i = atomicAdd(&g_irk_trace_n, 1ull);
+    if (!g_irk_trace || i >= g_irk_trace_cap) return;
+    unsigned smid;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    unsigned long long *r = g_irk_trace + 6 * i;
+    r[0] = ((unsigned long long)c << 32) | (unsigned long long)b;
+    r[1] = ((unsigned long long)smid << 48) | ((unsigned long long)blockIdx.x << 16) | threadIdx.x;
+    r[2] = tf;
+    r[3] = ts;
+    r[4] = irk_now();
+    r[5] = (unsigned long long)sweeps;
+}
+#endif
+
 // combine this chunk's max with the call's running max stored in stats[3]
 __device__ __forceinline__ void dhloc_store(int64_t *stats3, bool first_chunk, double dmax) {
     double prev = first_chunk ? 0.0 : __longlong_as_double(__ldcg(stats3));

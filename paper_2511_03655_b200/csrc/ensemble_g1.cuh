@@ -29,6 +29,12 @@ namespace irk {
 #define G1_BLOCK 64
 #endif
 constexpr int G1_THREADS = G1_BLOCK;
+#ifndef G1Q_PARK
+#define G1Q_PARK 0  // 1: park a blocked unit for its predecessor's lane (measured 92 -> 120 ms: the counter runs ahead)
+#endif
+#ifndef G1Q_HEAVY_MAXREG
+#define G1Q_HEAVY_MAXREG 240  // ens_g1q at <= 5 blocks per SM (launch geometry in irk_api.cu launch_g1q)
+#endif
 #ifndef G1_MAXREG
 #define G1_MAXREG 168    // measured best on config 2 (tools/variants.py): 128: 116 ms, 144: 136, 168: 107, 190+: 109-111
 #endif
@@ -345,8 +351,8 @@ __device__ __forceinline__ int64_t delta_bits8(const int64_t *e) {
     return t;
 }
 
-template <class P>
-__global__ void __maxnreg__(G1_MAXREG) ens_g1q_kernel(const __grid_constant__ EnsArgs a,
+template <class P, int MAXREG = G1_MAXREG>
+__global__ void __maxnreg__(MAXREG) ens_g1q_kernel(const __grid_constant__ EnsArgs a,
                                                      const __grid_constant__ QueueArgs qa,
                                                      const __grid_constant__ P prob) {
     constexpr int d = P::d, D = 2 * d;
@@ -372,6 +378,9 @@ __global__ void __maxnreg__(G1_MAXREG) ens_g1q_kernel(const __grid_constant__ En
     double hprev = 0.0, dhmax = 0.0;
     int k = 0;
     int32_t bb = 0;
+#ifdef IRK_TRACE
+    unsigned long long t_fetch = 0, t_start = 0;
+#endif
     for (;;) {
         if (b < 0) {  // ---- acquire the next unit (divergent, once per unit) ----
             if (u < 0) {
@@ -379,11 +388,32 @@ __global__ void __maxnreg__(G1_MAXREG) ens_g1q_kernel(const __grid_constant__ En
                 if (u >= total) break;
                 c = u / B;
                 bb = (int32_t)(u - c * B);
+#ifdef IRK_TRACE
+                t_fetch = irk_now();
+#endif
             }
             if (c > 0 && ld_acquire(&qa.progress[bb]) < c) {  // predecessor unit still running
+#if G1Q_PARK
+                // park the unit for the lane finishing (bb, c - 1) and fetch another one
+                // (hand-off protocol of ens_common.cuh: exactly one of the two runs it)
+                if (atomicCAS(&qa.orphan[bb], 0, (int)c) == 0) {
+                    __threadfence();
+                    if (!(ld_acquire(&qa.progress[bb]) >= c && atomicCAS(&qa.orphan[bb], (int)c, 0) == (int)c)) {
+                        u = -1;
+                        continue;
+                    }
+                } else {  // another unit of bb is parked already (rare): wait
+                    __nanosleep(1024);
+                    continue;
+                }
+#else
                 __nanosleep(1024);
                 continue;
+#endif
             }
+#ifdef IRK_TRACE
+            t_start = irk_now();
+#endif
             u = -1;
             b = bb;
             const int64_t c0 = c * qa.qchunk;
@@ -550,8 +580,37 @@ __global__ void __maxnreg__(G1_MAXREG) ens_g1q_kernel(const __grid_constant__ En
                 if (a.iters) a.iters[b] = (c == 0) ? sweeps : __ldcg(&a.iters[b]) + sweeps;
                 if (a.local_energy) dhloc_store(&a.stats[3 * B + b], c == 0, dhmax);
                 st_release(&qa.progress[b], (int32_t)(c + 1));
+#ifdef IRK_TRACE
+                irk_trace_unit(c, b, t_fetch, t_start, sweeps);
+#endif
+#if G1Q_PARK
+                // the next unit of this trajectory was parked for this lane: continue it
+                // from the registers (same arithmetic as reloading the stored state)
+                bool carry = false;
+                while (claim_orphan(qa, b, c + 1)) {
+                    ++c;
+                    if (finite) {
+                        carry = true;
+                        break;
+                    }
+                    st_release(&qa.progress[b], (int32_t)(c + 1));  // frozen trajectory: nothing to do
+                }
+                if (carry) {
+                    const int64_t c0 = c * qa.qchunk;
+                    len = (a.nsteps - c0 < qa.qchunk) ? a.nsteps - c0 : qa.qchunk;
+                    n = hits = sweeps = 0;
+                    dhmax = 0.0;
+#ifdef IRK_TRACE
+                    t_fetch = t_start = irk_now();
+#endif
+                } else {
+                    b = -1;
+                    continue;
+                }
+#else
                 b = -1;
                 continue;
+#endif
             }
         }
         // a4 (second half) / next step's a1: V_i = v + D(W_i., Lv), W = fin ? nu : mu

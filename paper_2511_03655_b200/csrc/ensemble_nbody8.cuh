@@ -57,9 +57,13 @@ __device__ __forceinline__ void n8_accel(const double *Q, double *A, const NBody
             const double dx = dsub(Q[3 * j], Q[3 * i]), dy = dsub(Q[3 * j + 1], Q[3 * i + 1]),
                          dz = dsub(Q[3 * j + 2], Q[3 * i + 2]);
             const double r2 = dfma(dz, dz, dfma(dy, dy, dfma(dx, dx, P.eps2)));
-            w[p] = EXACT ? ddiv(P.G, dmul(r2, dsqrt(r2)))
-                         : (G1 ? drcp_fast(dmul(r2, dsqrt_fast(r2, ok)), ok)  // G == 1: same bits
-                               : ddiv_fast(P.G, dmul(r2, dsqrt_fast(r2, ok)), ok));
+            if (!EXACT && G1) {  // G == 1: reciprocal form, one range predicate per pair (fp64.cuh)
+                bool unused = true;
+                ok = ok && weight_range_ok(r2);
+                w[p] = drcp_fast(dmul(r2, dsqrt_fast(r2, unused)), unused);
+            } else {
+                w[p] = EXACT ? ddiv(P.G, dmul(r2, dsqrt(r2))) : ddiv_fast(P.G, dmul(r2, dsqrt_fast(r2, ok)), ok);
+            }
         }
 #pragma unroll
     for (int i = 0; i < NB; ++i) {

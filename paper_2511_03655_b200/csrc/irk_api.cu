@@ -16,6 +16,12 @@
 
 #include "../../include/irk.h"
 #include "balance.cuh"
+#ifndef G1Q_UNITS
+#define G1Q_UNITS 16  // step chunks per trajectory of the ens_g1q work queue (config 2: 16 -> 81.4 ms, 12: 81.8, 32: 82.0, 8: 83.1)
+#endif
+#ifndef G1Q_MAX_BPS
+#define G1Q_MAX_BPS 0  // > 0: force the heavy ens_g1q kernel at this many blocks per SM (A/B builds); 0: auto
+#endif
 #include "ensemble_g1.cuh"
 #include "ensemble_g8.cuh"
 #include "ensemble_fo.cuh"
@@ -41,6 +47,7 @@ struct irk_ctx {
     int64_t balance = -1;  // IRK_OPT_BALANCE: -1 auto, 0 off, >0 chunk length
     int schedule = 0;      // IRK_OPT_SCHEDULE: 0 auto, 1 chunked launches, 2 persistent work queue
     int g1q_blocks_per_sm = 0;  // occupancy of the work-queue kernels (queried once)
+    int g1q_heavy_blocks_per_sm = 0;
     int chain_blocks_per_sm[5] = {0, 0, 0, 0, 0};
     int nbody_blocks_per_sm[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
     int fo_blocks_per_sm = 0;
@@ -532,7 +539,7 @@ EnsArgs ens_args(irk_ctx *c, double *y, double t0, char *ws, double *energy, int
 // (one unit per trajectory when every trajectory has its own slot, else ~32).
 template <class KernelPtr, class LaunchFn>
 int launch_queue(irk_ctx *c, KernelPtr kernel, int threads, int spb, int *bps_cache, EnsArgs &a, char *ws,
-                 cudaStream_t st, LaunchFn launch, int units = 32) {
+                 cudaStream_t st, LaunchFn launch, int units = 32, int max_bps = 0) {
     int rc;
     if (!*bps_cache &&
         (rc = cuda_check(c, cudaOccupancyMaxActiveBlocksPerMultiprocessor(bps_cache, kernel, threads, 0), "occupancy")))
@@ -540,7 +547,9 @@ int launch_queue(irk_ctx *c, KernelPtr kernel, int threads, int spb, int *bps_ca
     int dev = 0, sms = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    const int64_t resident_blocks = (int64_t)sms * (*bps_cache > 0 ? *bps_cache : 1);
+    int bps = *bps_cache > 0 ? *bps_cache : 1;
+    if (max_bps > 0 && bps > max_bps) bps = max_bps;
+    const int64_t resident_blocks = (int64_t)sms * bps;
     const int64_t need = (c->batch + spb - 1) / spb;
     const int64_t blocks = need < resident_blocks ? need : resident_blocks;
     irk::QueueArgs qa;
@@ -572,12 +581,39 @@ int launch_queue(irk_ctx *c, KernelPtr kernel, int threads, int spb, int *bps_ca
     return cuda_check(c, cudaGetLastError(), "advance_n launch");
 }
 
+// ens_g1q launch geometry.  The makespan of the queue is max(total work / lanes,
+// the slowest trajectory's serial chain): a trajectory's units run one after the
+// other, each at the per-lane speed of a loaded SM, so with lanes ~ batch the
+// slowest trajectory (config 2: 1.29x the mean sweeps) outlasts the average lane
+// and its successors' units are fetched early and wait (unit trace: 7.3 % of
+// lane time waiting, 7.4 % idle, tools/unit_trace.py).  Fewer resident lanes
+// shorten the chains (each lane gets a larger share of its SM's FP64 pipe) at
+// some cost in throughput: below 1.5 x the light kernel's resident lanes, the
+// kernel runs with 4-5 blocks of 64 per SM and 240 registers (config 2:
+// 92.2 -> 81.4 ms, with 16 units per trajectory instead of 32); above it, 6
+// blocks at 168 registers (B = 262,144 x 2,500 steps: 76.8 ms vs 85.1 at 4 blocks).
 template <class P>
 int launch_g1q(irk_ctx *c, const P &prob, EnsArgs &a, char *ws, cudaStream_t st) {
-    return launch_queue(c, irk::ens_g1q_kernel<P>, irk::G1_THREADS, irk::G1_THREADS, &c->g1q_blocks_per_sm, a, ws, st,
+    int dev = 0, sms = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    int &bps_light = c->g1q_blocks_per_sm;
+    if (!bps_light)
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps_light, irk::ens_g1q_kernel<P>, irk::G1_THREADS, 0);
+    const int64_t light_lanes = (int64_t)sms * (bps_light > 0 ? bps_light : 1) * irk::G1_THREADS;
+    if (G1Q_MAX_BPS == 0 && 2 * c->batch >= 3 * light_lanes)
+        return launch_queue(c, irk::ens_g1q_kernel<P>, irk::G1_THREADS, irk::G1_THREADS, &c->g1q_blocks_per_sm, a, ws,
+                            st, [&](const EnsArgs &aa, const irk::QueueArgs &qa, unsigned nb) {
+                                irk::ens_g1q_kernel<P><<<nb, irk::G1_THREADS, 0, st>>>(aa, qa, prob);
+                            }, G1Q_UNITS);
+    int64_t cap = (2 * c->batch) / (3 * (int64_t)sms * irk::G1_THREADS);
+    cap = cap < 4 ? 4 : (cap > 5 ? 5 : cap);
+    if (G1Q_MAX_BPS > 0) cap = G1Q_MAX_BPS;
+    auto heavy = irk::ens_g1q_kernel<P, G1Q_HEAVY_MAXREG>;
+    return launch_queue(c, heavy, irk::G1_THREADS, irk::G1_THREADS, &c->g1q_heavy_blocks_per_sm, a, ws, st,
                         [&](const EnsArgs &aa, const irk::QueueArgs &qa, unsigned nb) {
-                            irk::ens_g1q_kernel<P><<<nb, irk::G1_THREADS, 0, st>>>(aa, qa, prob);
-                        });
+                            heavy<<<nb, irk::G1_THREADS, 0, st>>>(aa, qa, prob);
+                        }, G1Q_UNITS, (int)cap);
 }
 
 // Stage-per-lane mappings (ensemble_g8.cuh): one launch, one group of G lanes per
@@ -1340,3 +1376,14 @@ void irk_destroy(irk_ctx *c) {
 }
 
 }  // extern "C"
+
+#ifdef IRK_TRACE
+// measurement builds only (tools/unit_trace.py): point the work-unit trace at a
+// device buffer of cap records (6 x uint64 each) and reset its counter
+extern "C" int irk_trace_set(void *buf, int64_t cap) {
+    unsigned long long *p = static_cast<unsigned long long *>(buf), n = 0, c = (unsigned long long)cap;
+    if (cudaMemcpyToSymbol(irk::g_irk_trace, &p, sizeof p) != cudaSuccess) return -1;
+    if (cudaMemcpyToSymbol(irk::g_irk_trace_n, &n, sizeof n) != cudaSuccess) return -1;
+    return cudaMemcpyToSymbol(irk::g_irk_trace_cap, &c, sizeof c) == cudaSuccess ? 0 : -1;
+}
+#endif

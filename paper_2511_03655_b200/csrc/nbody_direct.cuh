@@ -386,8 +386,27 @@ __global__ void __launch_bounds__(NBD_FORCE_THREADS, NBD_FORCE_MINB) nbd_force_k
             "}\n" ::"r"(smem_u32(&mbar))
             : "memory");
     }
-    // ---- the block's pair sums (pass 1 only if an operand left the fast-path range) ----
+    // ---- range pre-check: with every coordinate of the block's bodies j and i finite
+    // and below 2^290 in magnitude, eps^2 >= 2^-600 and 2^-100 <= G <= 2^100, every
+    // pair has eps^2 <= r2 < 2^600 (r2 is an fma chain of non-negative terms added to
+    // eps^2, rounding is monotone), so r2 * sqrt(r2) and the weight stay normal and
+    // the fast division / square root paths are valid for every pair: the per-pair
+    // range predicates can be skipped (same bits, nbd_force)
+    bool in_range = !act || (fabs(qx) < 0x1p290 && fabs(qy) < 0x1p290 && fabs(qz) < 0x1p290);
+    for (int t = threadIdx.x; t < 3 * nj; t += blockDim.x) in_range = in_range && fabs(sxyz[t]) < 0x1p290;
+    const bool unchecked = __syncthreads_and(in_range) && a.eps2 >= 0x1p-600 && a.G >= 0x1p-100 && a.G <= 0x1p100;
     double px = 0.0, py = 0.0, pz = 0.0;
+    if (unchecked) {
+        bool dummy = true;
+        if (act) nbd_pairs<false, G1>(sxyz, smass, nj, qx, qy, qz, a.G, a.eps2, px, py, pz, dummy);
+        if (!act) return;
+        double *P = a.part + ((int64_t)J * 8 + i) * dl;
+        P[3 * body] = px;
+        P[3 * body + 1] = py;
+        P[3 * body + 2] = pz;
+        return;
+    }
+    // ---- the block's pair sums (pass 1 only if an operand left the fast-path range) ----
     bool ok = true;
     if (act) nbd_pairs<false, G1>(sxyz, smass, nj, qx, qy, qz, a.G, a.eps2, px, py, pz, ok);
     if (__syncthreads_or(!ok)) {  // exact intrinsics, same bits, for the whole block

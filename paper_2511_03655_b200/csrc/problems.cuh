@@ -19,8 +19,16 @@ struct KeplerT {
     template <bool EXACT>
     __device__ __forceinline__ void accel(const double *q, double *a, double /*t*/, bool &ok) const {
         double r2 = dfma(q[0], q[0], dmul(q[1], q[1]));
-        double r3 = dmul(r2, EXACT ? dsqrt(r2) : dsqrt_fast(r2, ok));
-        double w = EXACT ? ddiv(GM, r3) : (UNIT_GM ? drcp_fast(r3, ok) : ddiv_fast(GM, r3, ok));
+        double r3, w;
+        if (!EXACT && UNIT_GM) {  // one range predicate for the whole chain (fp64.cuh)
+            bool unused = true;
+            ok = ok && weight_range_ok(r2);
+            r3 = dmul(r2, dsqrt_fast(r2, unused));
+            w = drcp_fast(r3, unused);
+        } else {
+            r3 = dmul(r2, EXACT ? dsqrt(r2) : dsqrt_fast(r2, ok));
+            w = EXACT ? ddiv(GM, r3) : (UNIT_GM ? drcp_fast(r3, ok) : ddiv_fast(GM, r3, ok));
+        }
         a[0] = -dmul(w, q[0]);
         a[1] = -dmul(w, q[1]);
     }
