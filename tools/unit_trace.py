@@ -63,7 +63,7 @@ def main():
     tf, ts, te, sw = r[:, 2], r[:, 3], r[:, 4], r[:, 5]
     t0 = tf.min()
     T = te.max() - t0
-    lanes = 148 * 384
+    lanes = int(len(np.unique(r[:, 1])))   # distinct (SM, block, thread) slots that ran units
     busy = (te - ts).sum() / (lanes * T)
     wait = (ts - tf).sum() / (lanes * T)
     bins = 50
