@@ -334,7 +334,7 @@ __global__ void __maxnreg__(FO8_MAXREG) ens_fo8_kernel(const __grid_constant__ E
 #pragma unroll
             for (int j = 1; j < 8; ++j) acc = dfma(Mu[8 * j], G[j * D + l], acc);
             Yn[l] = dadd(y[l], acc);
-            int64_t e = __double_as_longlong(dsub(Yn[l], Ys[l])) & 0x7fffffffffffffffLL;
+            int64_t e = dabs_bits(dsub(Yn[l], Ys[l]));
             e = (e > kInf) ? 0 : e;  // NaN-ignoring max
 #pragma unroll
             for (int off = 1; off < 8; off <<= 1) {

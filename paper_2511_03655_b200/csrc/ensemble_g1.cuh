@@ -332,7 +332,7 @@ namespace irk {
 __device__ __forceinline__ int64_t dbits(double x) { return __double_as_longlong(x); }
 // |a - b| as bits (NaN stays above +inf: a NaN-ignoring max is taken separately)
 __device__ __forceinline__ int64_t absdiff_bits(double a, double b) {
-    return dbits(dsub(a, b)) & 0x7fffffffffffffffLL;
+    return dabs_bits(dsub(a, b));  // integer-pipe mask (fp64.cuh)
 }
 __device__ __forceinline__ int64_t imax64(int64_t a, int64_t b) { return a > b ? a : b; }
 __device__ __forceinline__ int64_t imin64(int64_t a, int64_t b) { return a < b ? a : b; }

@@ -174,7 +174,7 @@ __global__ void __maxnreg__(G8_MAXREG) ens_gs_kernel(const __grid_constant__ Ens
 #pragma unroll
             for (int t = 0; t < SPL; ++t) {
                 Qs[t][l] = dadd(q[l], acc[t]);
-                int64_t et = __double_as_longlong(dsub(Qs[t][l], Qold[t][l])) & 0x7fffffffffffffffLL;
+                int64_t et = dabs_bits(dsub(Qs[t][l], Qold[t][l]));
                 et = (et > kInfBits) ? 0 : et;  // NaN-ignoring max (canonical left-to-right form)
                 e = (et > e) ? et : e;
                 Qold[t][l] = Qs[t][l];

@@ -29,8 +29,10 @@ struct KeplerT {
             r3 = dmul(r2, EXACT ? dsqrt(r2) : dsqrt_fast(r2, ok));
             w = EXACT ? ddiv(GM, r3) : (UNIT_GM ? drcp_fast(r3, ok) : ddiv_fast(GM, r3, ok));
         }
-        a[0] = -dmul(w, q[0]);
-        a[1] = -dmul(w, q[1]);
+        // -(w q) as (-w) q: the same bits (round to nearest is sign-symmetric), and the
+        // negation is an operand modifier of the DMUL instead of a separate DADD
+        a[0] = dmul(-w, q[0]);
+        a[1] = dmul(-w, q[1]);
     }
     __device__ __forceinline__ double energy(const double *q, const double *v) const {
         Neumaier n;
