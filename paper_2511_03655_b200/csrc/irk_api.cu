@@ -88,15 +88,17 @@ constexpr size_t kHeader = 64;
 #define IRK_G8_AUTO_MAX 6144
 #endif
 #ifndef IRK_G4_AUTO_MAX
-#define IRK_G4_AUTO_MAX 16384
+#define IRK_G4_AUTO_MAX 12288
 #endif
 #ifndef IRK_G2_AUTO_MAX
-#define IRK_G2_AUTO_MAX 24576
+#define IRK_G2_AUTO_MAX 0  // g2 is not chosen by auto any more (g1 on 2 blocks per SM beats it)
 #endif
-// IRK_OPT_MAPPING auto (Kepler, HH): g8 up to kG8AutoMaxBatch, g4 up to kG4AutoMaxBatch, g2 up to
-// kG2AutoMaxBatch, then g1 (tools/mapping_ab.py, config-2 generator, 2,000 steps, g1/g2/g4/g8 ms:
-// 8,192: 8.73/7.35/5.87/6.01; 12,288: 8.92/8.89/7.09/9.92; 16,384: 8.94/9.11/8.86/11.3;
-// 24,576: 12.7/11.95/13.6/15.9; 32,768: 12.8/15.1/16.4/20.9)
+// IRK_OPT_MAPPING auto (Kepler, HH): g8 up to kG8AutoMaxBatch, g4 up to kG4AutoMaxBatch, then g1
+// (ens_g1q, launch geometry in launch_g1q).  Measured with tools/ab.py, config-2 generator,
+// 10,000 steps (profiles/r2/ab_mapping_crossover.json), g1 / g2 / g4 / g8 ms:
+// 4,096: 38.9/31.2/22.2/19.3; 6,144: 38.9/31.6/26.8/23.9; 8,192: 38.7/31.5/27.0/29.6;
+// 12,288: 39.5/42.5/34.7/45.0; 16,384: 39.2/42.9/56.1/54.3; 24,576: 43.2/56.8/67.4/76.6
+// (g1 at 2 blocks per SM from 16,384 on).
 constexpr int64_t kG8AutoMaxBatch = IRK_G8_AUTO_MAX;
 constexpr int64_t kG4AutoMaxBatch = IRK_G4_AUTO_MAX;
 constexpr int64_t kG2AutoMaxBatch = IRK_G2_AUTO_MAX;
@@ -583,15 +585,16 @@ int launch_queue(irk_ctx *c, KernelPtr kernel, int threads, int spb, int *bps_ca
 
 // ens_g1q launch geometry.  The makespan of the queue is max(total work / lanes,
 // the slowest trajectory's serial chain): a trajectory's units run one after the
-// other, each at the per-lane speed of a loaded SM, so with lanes ~ batch the
-// slowest trajectory (config 2: 1.29x the mean sweeps) outlasts the average lane
-// and its successors' units are fetched early and wait (unit trace: 7.3 % of
-// lane time waiting, 7.4 % idle, tools/unit_trace.py).  Fewer resident lanes
-// shorten the chains (each lane gets a larger share of its SM's FP64 pipe) at
-// some cost in throughput: below 1.5 x the light kernel's resident lanes, the
-// kernel runs with 4-5 blocks of 64 per SM and 240 registers (config 2:
-// 92.2 -> 81.4 ms, with 16 units per trajectory instead of 32); above it, 6
-// blocks at 168 registers (B = 262,144 x 2,500 steps: 76.8 ms vs 85.1 at 4 blocks).
+// other, each at the per-lane speed of its SM, so with lanes ~ batch the slowest
+// trajectory (config 2: 1.29x the mean sweeps) outlasts the average lane and its
+// successors' units are fetched early and wait (unit trace of the round-1 launch:
+// 7.3 % of lane time waiting, 7.4 % idle; tools/unit_trace.py).  Fewer resident
+// lanes shorten the chains (each lane gets a larger share of its SM's FP64 pipe)
+// at some cost in throughput, so below 1.5 x the light kernel's resident lanes the
+// kernel runs 2-4 blocks of 64 per SM (from the batch) at up to 240 registers
+// (config 2: 92.2 -> 81.4 ms, with 16 units per trajectory instead of 32); above
+// it, 6 blocks at 168 registers (B = 262,144 x 2,500 steps: 76.8 ms vs 85.1 ms at
+// 4 blocks).  Bitwise-neutral: every unit does the same arithmetic.
 template <class P>
 int launch_g1q(irk_ctx *c, const P &prob, EnsArgs &a, char *ws, cudaStream_t st) {
     int dev = 0, sms = 0;
@@ -606,8 +609,11 @@ int launch_g1q(irk_ctx *c, const P &prob, EnsArgs &a, char *ws, cudaStream_t st)
                             st, [&](const EnsArgs &aa, const irk::QueueArgs &qa, unsigned nb) {
                                 irk::ens_g1q_kernel<P><<<nb, irk::G1_THREADS, 0, st>>>(aa, qa, prob);
                             }, G1Q_UNITS);
-    int64_t cap = (2 * c->batch) / (3 * (int64_t)sms * irk::G1_THREADS);
-    cap = cap < 4 ? 4 : (cap > 5 ? 5 : cap);
+    // blocks per SM from the batch (measured, config-2 generator, 10,000 steps, ms at
+    // 2 / 3 / 4 blocks: 24,576: 43.2/60.7/60.0; 32,768: 56.5/59.9/60.5; 40,960:
+    // 70.2/63.6/64.7; 49,152: 84.0/71.3/66.1; 57,344: 97.7/82.1/71.2; 65,536: -/-/80.1)
+    int64_t cap = c->batch / ((int64_t)sms * 83);
+    cap = cap < 2 ? 2 : (cap > 4 ? 4 : cap);
     if (G1Q_MAX_BPS > 0) cap = G1Q_MAX_BPS;
     auto heavy = irk::ens_g1q_kernel<P, G1Q_HEAVY_MAXREG>;
     return launch_queue(c, heavy, irk::G1_THREADS, irk::G1_THREADS, &c->g1q_heavy_blocks_per_sm, a, ws, st,

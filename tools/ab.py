@@ -3,7 +3,7 @@
 repetition (state reset and L2 flush outside the events), and a digest of the
 final state so that every build must give the same bits.
 
-python tools/ab.py --libs base=lib/variants/libirk_base.so,new=lib/libirk.so \
+python tools/ab.py --libs base=lib/variants/libirk_base.so,new=lib/libirk.so[@mapping] \
                    --configs 2,3:5000,5:100 [--reps 3] [--out gpurun_out/ab.json]
 A config is `i`, `i:nsteps` or `i:nsteps:batch`.
 """
@@ -23,7 +23,7 @@ kw = {{}}
 if {nsteps}: kw['nsteps'] = {nsteps}
 if {batch}: kw['batch'] = {batch}
 w = wl.config({cfg}, **kw)
-ig = irk.Integrator(w.problem, w.dim, w.h, w.nsteps, w.batch, w.params)
+ig = irk.Integrator(w.problem, w.dim, w.h, w.nsteps, w.batch, w.params, mapping=int(os.environ.get('IRK_AB_MAPPING', '0')))
 y0 = torch.tensor(w.y, dtype=torch.float64, device='cuda'); Y = torch.empty_like(y0)
 ws = ig.new_workspace(); it = torch.zeros(w.batch, dtype=torch.int64, device='cuda')
 flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device='cuda')
@@ -57,8 +57,9 @@ def main():
         for rep in range(a.reps):
             order = list(libs) if rep % 2 == 0 else list(libs)[::-1]
             for n in order:
-                env = dict(os.environ, IRK_LIB_OVERRIDE=os.path.abspath(os.path.join(ROOT, libs[n])
-                                                                        if not os.path.isabs(libs[n]) else libs[n]))
+                libpath, _, mp = libs[n].partition("@")   # name=path[@mapping]
+                env = dict(os.environ, IRK_AB_MAPPING=mp or "0", IRK_LIB_OVERRIDE=os.path.abspath(os.path.join(ROOT, libpath)
+                                                                        if not os.path.isabs(libpath) else libpath))
                 code = CHILD.format(root=ROOT, cfg=int(cfg), nsteps=int(ns or 0), batch=int(bt or 0), calls=a.calls)
                 p = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, env=env)
                 if p.returncode:
