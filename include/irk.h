@@ -20,7 +20,12 @@
  *  - All device work is enqueued on `stream` (a cudaStream_t; NULL = legacy
  *    default stream) and is asynchronous: buffers must stay alive until the
  *    stream is synchronised.  Functions that must read device results
- *    (irk_stats) synchronise the stream themselves.
+ *    (irk_stats) synchronise the stream themselves.  Exception: irk_integrate
+ *    on IRK_NBODY_DIRECT synchronises `stream` at its start (to see whether the
+ *    system diverged in an earlier call), after every energy-sample segment of
+ *    its device-side sweep loop, after every sweep when IRK_OPT_DEVICE_LOOP = 0,
+ *    and at the end of an IRK_OPT_EXCHANGE = 1 call (DESIGN.md section 6,
+ *    nbody_direct, "Synchronisation").
  *  - Errors: functions return an irk_status; argument errors are detected
  *    synchronously and leave every buffer untouched.  irk_last_error() gives a
  *    message.  A ctx is not thread-safe; distinct ctxs are independent.
