@@ -32,6 +32,9 @@ constexpr int G1_THREADS = G1_BLOCK;
 #ifndef G1Q_PARK
 #define G1Q_PARK 0  // 1: park a blocked unit for its predecessor's lane (measured 92 -> 120 ms: the counter runs ahead)
 #endif
+#ifndef G1Q_QREG
+#define G1Q_QREG 1  // the heavy ens_g1q keeps the stage positions in registers
+#endif
 #ifndef G1Q_HEAVY_MAXREG
 #define G1Q_HEAVY_MAXREG 240  // ens_g1q at <= 5 blocks per SM (launch geometry in irk_api.cu launch_g1q)
 #endif
@@ -365,7 +368,16 @@ __global__ void __maxnreg__(MAXREG) ens_g1q_kernel(const __grid_constant__ EnsAr
     for (int e = threadIdx.x; e < 128; e += blockDim.x)
         sW[(e < 64) ? e : kNuOff + e - 64] = (e < 64) ? (&c_mu[0][0])[e] : (&c_nu[0][0])[e - 64];
     __syncthreads();
-    __shared__ double sQ[8 * d][G1_THREADS], sL[8 * d][G1_THREADS];
+    // Q^[k] (read by the RHS and, as Q^[k-1], by the next sweep's Delta): in registers
+    // when the register budget allows (the <= 5-blocks-per-SM instantiation), else in
+    // shared memory [element][thread] (conflict-free)
+    constexpr bool QREG = MAXREG >= 200 && G1Q_QREG;
+    __shared__ double sQ[QREG ? 1 : 8 * d][G1_THREADS], sL[8 * d][G1_THREADS];
+    double Qr[8][d];
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int l = 0; l < d; ++l) Qr[i][l] = 0.0;
     __shared__ int64_t sM[d][G1_THREADS], sP[d][G1_THREADS];
     const int tx = threadIdx.x;
     const int64_t n0 = *a.n_done;
@@ -489,8 +501,13 @@ __global__ void __maxnreg__(MAXREG) ens_g1q_kernel(const __grid_constant__ EnsAr
                         acc = dfma(w[jj].y, Lq[2 * jj + 1][l], acc);
                     }
                     const double qn = dadd(q[l], acc);
-                    ev[l][i] = absdiff_bits(qn, sQ[i * d + l][tx]);  // garbage at k = 1, unused
-                    sQ[i * d + l][tx] = qn;
+                    if (QREG) {
+                        ev[l][i] = absdiff_bits(qn, Qr[i][l]);  // garbage at k = 1, unused
+                        Qr[i][l] = qn;
+                    } else {
+                        ev[l][i] = absdiff_bits(qn, sQ[i * d + l][tx]);
+                        sQ[i * d + l][tx] = qn;
+                    }
                 }
             }
 #pragma unroll
@@ -516,15 +533,20 @@ __global__ void __maxnreg__(MAXREG) ens_g1q_kernel(const __grid_constant__ EnsAr
             for (int i = 0; i < 8; ++i) {
                 double Qi[d];
 #pragma unroll
-                for (int l = 0; l < d; ++l) Qi[l] = sQ[i * d + l][tx];
+                for (int l = 0; l < d; ++l) Qi[l] = QREG ? Qr[i][l] : sQ[i * d + l][tx];
                 prob.template accel<false>(Qi, Lv[i], dadd(tn1, dmul(c_c[i], a.h)), ok);
             }
             if (!ok) {  // some stage needs the exact slow path of div/sqrt: redo all, same bits
+                if (QREG)  // through shared memory (a register array indexed in a rolled loop would
+#pragma unroll             // put Qr in local memory for the whole kernel)
+                    for (int i = 0; i < 8; ++i)
+#pragma unroll
+                        for (int l = 0; l < d; ++l) sL[i * d + l][tx] = Qr[i][l];
 #pragma unroll 1
                 for (int i = 0; i < 8; ++i) {
                     double Qi[d], Fi[d];
 #pragma unroll
-                    for (int l = 0; l < d; ++l) Qi[l] = sQ[i * d + l][tx];
+                    for (int l = 0; l < d; ++l) Qi[l] = QREG ? sL[i * d + l][tx] : sQ[i * d + l][tx];
                     prob.template accel<true>(Qi, Fi, dadd(tn1, dmul(c_c[i], a.h)), ok);
 #pragma unroll
                     for (int l = 0; l < d; ++l) sL[i * d + l][tx] = Fi[l];
