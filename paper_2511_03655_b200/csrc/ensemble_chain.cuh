@@ -45,19 +45,41 @@ __device__ double fpu_energy(const double *q, const double *v, double beta) {
 // lives at s*32 + L, so own-site and neighbour-site accesses of a warp hit 32
 // consecutive doubles (conflict-free; the site-major layout was 2-way conflicted
 // for SPL = 2).
-template <int SPL>
-__device__ __forceinline__ int ch_slot(int site) { return (site % SPL) * 32 + site / SPL; }
+template <int SPL, int WPC = 1>
+__device__ __forceinline__ int ch_slot(int site) { return (site % SPL) * (32 * WPC) + site / SPL; }
 
-// One warp integrates chain b over the call-local steps [c0, c0 + nsteps).
-template <int SPL>
+// barrier over the WPC warps of one chain (WPC > 1: the block is one chain)
+template <int WPC>
+__device__ __forceinline__ void chain_sync() {
+    if (WPC == 1) __syncwarp();
+    else __syncthreads();
+}
+
+// WPC warps (one warp when WPC = 1) integrate chain b over the call-local steps
+// [c0, c0 + nsteps); thread tid of the chain owns sites tid*SPL .. tid*SPL+SPL-1.
+// WPC > 1 (small batches: more lanes per chain, shorter sweeps): the block is the
+// chain, the stage tile and the votes are exchanged with block barriers.
+template <int SPL, int WPC = 1>
 __device__ __forceinline__ void chain_unit(const EnsArgs &a, const double beta, const int64_t b, const int64_t c0,
-                                           const int64_t nsteps, double (*sQ)[32 * SPL], double *sQV,
-                                           const double (*sW)[64]) {
-    constexpr int N = 32 * SPL, d = N, D = 2 * N;
+                                           const int64_t nsteps, double (*sQ)[32 * SPL * WPC], double *sQV,
+                                           const double (*sW)[64], int *sVote = nullptr) {
+    constexpr int N = 32 * SPL * WPC, d = N, D = 2 * N, TPC = 32 * WPC;
     const unsigned FULL = 0xffffffffu;
     const int64_t B = a.batch;
-    const int lane = threadIdx.x & 31;
+    const int lane = threadIdx.x % TPC;  // thread index within the chain
+    const int wic = lane >> 5;           // warp index within the chain
     const int s0 = lane * SPL;
+    // AND of a per-warp vote over the chain's warps (every thread calls it)
+    auto chain_all = [&](bool warp_vote) -> bool {
+        if (WPC == 1) return warp_vote;
+        if ((lane & 31) == 0) sVote[wic] = warp_vote ? 1 : 0;
+        chain_sync<WPC>();
+        bool all = true;
+#pragma unroll
+        for (int w = 0; w < WPC; ++w) all = all && sVote[w] != 0;
+        chain_sync<WPC>();  // votes read before the next write
+        return all;
+    };
 
     double q[SPL], v[SPL];
 #pragma unroll
@@ -76,14 +98,14 @@ __device__ __forceinline__ void chain_unit(const EnsArgs &a, const double beta, 
             sQV[s0 + s] = q[s];
             sQV[N + s0 + s] = v[s];
         }
-        __syncwarp();
+        chain_sync<WPC>();
         if (lane == 0) {
             const double hn = fpu_energy<N>(sQV, sQV + N, beta);
             if (idx >= 0) a.energy[idx * B + b] = hn;
             if (track) dhloc_update(hn, hprev, dhmax);
             else hprev = hn;
         }
-        __syncwarp();
+        chain_sync<WPC>();
     };
     if ((sample && c0 == 0) || a.local_energy) energy_at((sample && c0 == 0) ? 0 : -1, false);
     if (bad > 0 || nsteps == 0) {
@@ -132,7 +154,7 @@ __device__ __forceinline__ void chain_unit(const EnsArgs &a, const double beta, 
             for (int j = 1; j < 8; ++j) sLq[s] = dadd(sLq[s], Lq[j][s]);
             delta[s] = 0.0;
         }
-        __syncwarp();  // previous sweep's neighbour reads of sQ are done
+        chain_sync<WPC>();  // previous sweep's neighbour reads of sQ are done
         {
             const double2 *M = reinterpret_cast<const double2 *>(&c_mu[0][0]);
 #pragma unroll
@@ -150,9 +172,9 @@ __device__ __forceinline__ void chain_unit(const EnsArgs &a, const double beta, 
                         acc = dfma(w[jj].y, Lq[2 * jj + 1][s], acc);
                     }
                     const double qn = dadd(q[s], acc);
-                    const double e = dabs(dsub(qn, sQ[i][s * 32 + lane]));
+                    const double e = dabs(dsub(qn, sQ[i][s * TPC + lane]));
                     delta[s] = (e > delta[s]) ? e : delta[s];
-                    sQ[i][s * 32 + lane] = qn;
+                    sQ[i][s * TPC + lane] = qn;
                 }
             }
         }
@@ -167,19 +189,21 @@ __device__ __forceinline__ void chain_unit(const EnsArgs &a, const double beta, 
                 ok_lane = ok_lane && oks;
             }
         }
-        const bool all_ok = __all_sync(FULL, ok_lane);  // every lane votes (k is warp-uniform here)
+        // every lane votes (k is chain-uniform here); the chain barrier inside
+        // chain_all (or the warp barrier) also publishes this sweep's sQ writes
+        const bool all_ok = chain_all(__all_sync(FULL, ok_lane));
         const bool stop = (k >= 2) && all_ok;
-        __syncwarp();
+        if (WPC == 1) __syncwarp();
         // a3: bond forces of the lane's sites for every stage
         double Lv[8][SPL];
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
             const double *Qi = sQ[i];
             double qs[SPL + 2];
-            qs[0] = (s0 == 0) ? 0.0 : Qi[ch_slot<SPL>(s0 - 1)];
+            qs[0] = (s0 == 0) ? 0.0 : Qi[ch_slot<SPL, WPC>(s0 - 1)];
 #pragma unroll
-            for (int s = 0; s < SPL; ++s) qs[s + 1] = Qi[s * 32 + lane];
-            qs[SPL + 1] = (s0 + SPL == N) ? 0.0 : Qi[ch_slot<SPL>(s0 + SPL)];
+            for (int s = 0; s < SPL; ++s) qs[s + 1] = Qi[s * TPC + lane];
+            qs[SPL + 1] = (s0 + SPL == N) ? 0.0 : Qi[ch_slot<SPL, WPC>(s0 + SPL)];
             double f[SPL + 1];
 #pragma unroll
             for (int t = 0; t <= SPL; ++t) f[t] = fpu_bond(dsub(qs[t + 1], qs[t]), beta);
@@ -198,7 +222,7 @@ __device__ __forceinline__ void chain_unit(const EnsArgs &a, const double beta, 
                 v[s] = dadd(v[s], sv);
                 finite = finite && isfinite(q[s]) && isfinite(v[s]);
             }
-            finite = __all_sync(FULL, finite);
+            finite = chain_all(__all_sync(FULL, finite));
             ++n;
             sweeps += k;
             hits += stop ? 0 : 1;
@@ -273,6 +297,24 @@ __global__ void __maxnreg__(CH_MAXREG) ens_chain_kernel(const __grid_constant__ 
     const int64_t b = a.perm ? (int64_t)a.perm[slot] : slot;
     if (b < 0 || b >= a.batch) return;   // warp-uniform
     chain_unit<SPL>(a, beta, b, a.c0, a.nsteps, sQ[cib], sQV[cib], sW);
+}
+
+// Small batches: WPC warps per chain, one chain per block (SPL * WPC * 32 = N), a
+// single launch over the whole call.  Half (WPC = 2) the sites per lane, so a sweep
+// of one chain is shorter: the mapping for the per-GPU shares of strong scaling.
+template <int SPL, int WPC>
+__global__ void __launch_bounds__(32 * WPC) ens_chainw_kernel(const __grid_constant__ EnsArgs a, const double beta) {
+    constexpr int N = 32 * SPL * WPC;
+    __shared__ __align__(16) double sW[2][64];
+    __shared__ double sQ[8][N];
+    __shared__ double sQV[2 * N];
+    __shared__ int sVote[WPC];
+    for (int e = threadIdx.x; e < 128; e += blockDim.x)
+        sW[e >> 6][e & 63] = (e < 64) ? (&c_mu[0][0])[e] : (&c_nu[0][0])[e - 64];
+    __syncthreads();
+    const int64_t b = blockIdx.x;
+    if (b >= a.batch) return;  // block-uniform
+    chain_unit<SPL, WPC>(a, beta, b, a.c0, a.nsteps, sQ, sQV, sW, sVote);
 }
 
 // Persistent work-queue version (IRK_OPT_SCHEDULE 0/2; see ens_g1q): every warp

@@ -84,6 +84,9 @@ constexpr size_t kHeader = 64;
 #ifndef IRK_UNIT_G
 #define IRK_UNIT_G 1  // G = 1 / GM = 1 kernels use the reciprocal form of the division (fp64.cuh drcp_fast)
 #endif
+#ifndef IRK_CHAINW_MAX
+#define IRK_CHAINW_MAX 384  // FPU chains: two warps per chain up to this batch (20,000 steps, 1 / 2 warps: 256 chains 59.0 / 51.1 ms, 512: 59.3 / 65.1, 1,024: 99.9 / 112.5)
+#endif
 #ifndef IRK_G8_AUTO_MAX
 #define IRK_G8_AUTO_MAX 6144
 #endif
@@ -754,6 +757,20 @@ int launch_nbody_t(irk_ctx *c, double *y, double t0, char *ws, double *energy, i
 template <int SPL>
 int launch_chain_t(irk_ctx *c, double *y, double t0, char *ws, double *energy, int64_t *iters, cudaStream_t st) {
     EnsArgs a = ens_args(c, y, t0, ws, energy, iters);
+    // small batches (strong-scaling shares): two warps per chain, one launch
+    if (SPL % 2 == 0 && c->schedule == 0 && c->batch <= IRK_CHAINW_MAX) {
+        constexpr int SPLW = SPL / 2 > 0 ? SPL / 2 : 1;
+        a.nsteps = c->nsteps;
+        a.c0 = 0;
+        a.csweeps = nullptr;
+        a.perm = nullptr;
+        a.nslots = c->batch;
+        irk::ens_chainw_kernel<SPLW, 2><<<(unsigned)c->batch, 64, 0, st>>>(a, c->params[0]);
+        int rc = cuda_check(c, cudaGetLastError(), "ens_chainw launch");
+        if (rc) return rc;
+        advance_n_kernel<<<1, 1, 0, st>>>(reinterpret_cast<int64_t *>(ws), c->nsteps);
+        return cuda_check(c, cudaGetLastError(), "advance_n launch");
+    }
     constexpr int CPB = irk::CH_THREADS / 32;
     const int64_t blocks = (c->batch + CPB - 1) / CPB;
     const double beta = c->params[0];

@@ -127,3 +127,20 @@ def test_binding_rejects_bad_buffers(irk):
             ig.energy(Y, out=torch.zeros(w.batch, dtype=torch.float32, device="cuda"))
         ig.integrate(Y, ws, energy=E, iters=it)   # the good call still works
         torch.cuda.synchronize()
+
+
+# ------------------------------------------------------ FPU chains, two warps per chain
+@pytest.mark.parametrize("N,batch", [(64, 37), (128, 20)])
+def test_fpu_two_warps_per_chain(irk, orc, N, batch):
+    """Small batches run the FPU chain with two warps per chain (ens_chainw,
+    IRK_CHAINW_MAX): bitwise the oracle, with energy samples, and the same bits as
+    the one-warp chunked kernel (IRK_OPT_SCHEDULE = 1)."""
+    w = wl.fpu_ensemble(batch=batch, nsteps=600, N=N)
+    g = run_gpu(irk, w, energy_every=100)
+    o = orc.integrate(w.problem, w.y, w.params, w.h, w.nsteps, energy_every=100)
+    assert_parity(g, o, energy=True)
+    with irk.Integrator(w.problem, w.dim, w.h, w.nsteps, w.batch, w.params, schedule=1) as ig:
+        Y = torch.tensor(w.y, dtype=torch.float64, device="cuda")
+        ig.integrate(Y, ig.new_workspace())
+        torch.cuda.synchronize()
+        assert np.array_equal(Y.cpu().numpy(), g["y"])
