@@ -378,7 +378,13 @@ __global__ void __maxnreg__(MAXREG) ens_g1q_kernel(const __grid_constant__ EnsAr
     for (int i = 0; i < 8; ++i)
 #pragma unroll
         for (int l = 0; l < d; ++l) Qr[i][l] = 0.0;
-    __shared__ int64_t sM[d][G1_THREADS], sP[d][G1_THREADS];
+    // stop-test state (m, p) per component: registers in the heavy instantiation
+    __shared__ int64_t sM[QREG ? 1 : d][G1_THREADS], sP[QREG ? 1 : d][G1_THREADS];
+    int64_t rM[d], rP[d];
+#pragma unroll
+    for (int l = 0; l < d; ++l) rM[l] = rP[l] = 0x7ff0000000000000LL;
+#define G1Q_M(l) (*(QREG ? &rM[l] : &sM[l][tx]))
+#define G1Q_P(l) (*(QREG ? &rP[l] : &sP[l][tx]))
     const int tx = threadIdx.x;
     const int64_t n0 = *a.n_done;
     const bool sample = (a.energy != nullptr) && (a.energy_every > 0);
@@ -464,7 +470,7 @@ __global__ void __maxnreg__(MAXREG) ens_g1q_kernel(const __grid_constant__ EnsAr
                     }
             }
 #pragma unroll
-            for (int l = 0; l < d; ++l) sM[l][tx] = sP[l][tx] = kInfBits;
+            for (int l = 0; l < d; ++l) G1Q_M(l) = G1Q_P(l) = kInfBits;
             n = hits = sweeps = 0;
             k = 0;
         }
@@ -516,10 +522,10 @@ __global__ void __maxnreg__(MAXREG) ens_g1q_kernel(const __grid_constant__ EnsAr
         if (k >= 2) {  // a5, reading R2 (Delta^[k] exists from k = 2), on the bit patterns
 #pragma unroll
             for (int l = 0; l < d; ++l) {
-                const int64_t pl = sP[l][tx], ml = sM[l][tx];
+                const int64_t pl = G1Q_P(l), ml = G1Q_M(l);
                 const bool ok = (delta[l] == 0) || (ml <= imin64(delta[l], pl));
-                sM[l][tx] = imin64(pl, ml);
-                sP[l][tx] = delta[l];
+                G1Q_M(l) = imin64(pl, ml);
+                G1Q_P(l) = delta[l];
                 stop = stop && ok;
             }
         }
@@ -578,7 +584,7 @@ __global__ void __maxnreg__(MAXREG) ens_g1q_kernel(const __grid_constant__ EnsAr
             hits += stop ? 0 : 1;
             k = 0;
 #pragma unroll
-            for (int l = 0; l < d; ++l) sM[l][tx] = sP[l][tx] = kInfBits;
+            for (int l = 0; l < d; ++l) G1Q_M(l) = G1Q_P(l) = kInfBits;
             const int64_t nloc = c * qa.qchunk + n;  // call-local step index just completed
             if (sample && (nloc % a.energy_every) == 0)
                 a.energy[(nloc / a.energy_every) * B + b] = prob.energy(q, v);
@@ -658,6 +664,9 @@ __global__ void __maxnreg__(MAXREG) ens_g1q_kernel(const __grid_constant__ EnsAr
         }
     }
 }
+
+#undef G1Q_M
+#undef G1Q_P
 
 // First-order mode (Eqs. IRK_init / IRK_FP) for the per-thread
 // problems: all D = 2d components are extrapolated (a1 over y), each sweep
