@@ -519,14 +519,16 @@ __global__ void __maxnreg__(MAXREG) ens_g1q_kernel(const __grid_constant__ EnsAr
 #pragma unroll
             for (int l = 0; l < d; ++l) delta[l] = delta_bits8(ev[l]);
         }
-        if (k >= 2) {  // a5, reading R2 (Delta^[k] exists from k = 2), on the bit patterns
+        {   // a5, reading R2 (Delta^[k] exists from k = 2), on the bit patterns; branch-free
+            // (selects) so that lanes at k = 1 and k >= 2 do not diverge
+            const bool k2 = k >= 2;
 #pragma unroll
             for (int l = 0; l < d; ++l) {
                 const int64_t pl = G1Q_P(l), ml = G1Q_M(l);
                 const bool ok = (delta[l] == 0) || (ml <= imin64(delta[l], pl));
-                G1Q_M(l) = imin64(pl, ml);
-                G1Q_P(l) = delta[l];
-                stop = stop && ok;
+                G1Q_M(l) = k2 ? imin64(pl, ml) : ml;
+                G1Q_P(l) = k2 ? delta[l] : pl;
+                stop = stop && ok;   // (stop starts as k >= 2)
             }
         }
         // a3 + a4 (first half): F_i = g(Q_i, t_i) ; Lv_i = hb_i F_i, all eight stages in flight
