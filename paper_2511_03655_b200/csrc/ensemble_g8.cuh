@@ -223,15 +223,17 @@ __global__ void __maxnreg__(G8_MAXREG) ens_gs_kernel(const __grid_constant__ Ens
 #endif
         // the stop test after the right-hand sides: the RHS does not need it, so the
         // Delta shuffles and the RHS chains share one basic block and overlap
-        if (k >= 2) {  // reading R2, on the bit patterns as in ens_g1q
+        {   // reading R2, on the bit patterns as in ens_g1q; branch-free so
+            // that groups at k = 1 and k >= 2 do not diverge
+            const bool k2 = k >= 2;
 #pragma unroll
             for (int l = 0; l < d; ++l) {
                 const int64_t e = delta[l];
                 const int64_t mn = (e < p[l]) ? e : p[l];
                 const bool ok = (e == 0) || (m[l] <= mn);
-                m[l] = (p[l] < m[l]) ? p[l] : m[l];
-                p[l] = e;
-                stop = stop && ok;
+                m[l] = k2 ? ((p[l] < m[l]) ? p[l] : m[l]) : m[l];
+                p[l] = k2 ? e : p[l];
+                stop = stop && ok;  // (stop starts as k >= 2)
             }
         }
         const bool fin = live && (stop || k >= a.max_iters);
