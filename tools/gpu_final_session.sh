@@ -11,3 +11,4 @@ timeout 900 ncu --set full --clock-control none --import-source on -k regex:ens_
 ncu -i gpurun_out/g1q_final.ncu-rep --page raw --csv > gpurun_out/g1q_final_raw.csv 2>/dev/null
 ncu -i gpurun_out/g1q_final.ncu-rep --page source --csv --print-source cuda,sass > gpurun_out/g1q_final_src.csv 2>/dev/null
 rm -f gpurun_out/g1q_final.ncu-rep
+timeout 1200 python tools/strong_scaling.py gpurun_out/strong_scaling_final.json > gpurun_out/strong_scaling_final.log 2>&1; echo ss rc=$?
