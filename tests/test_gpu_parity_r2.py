@@ -144,3 +144,16 @@ def test_fpu_two_warps_per_chain(irk, orc, N, batch):
         ig.integrate(Y, ig.new_workspace())
         torch.cuda.synchronize()
         assert np.array_equal(Y.cpu().numpy(), g["y"])
+
+
+def test_work_queue_int32_guard(irk):
+    """Work-queue chunk indices are int32 (progress / orphan words): a call whose
+    step-chunk count reaches 2^31 - 1 is refused with IRK_E_ARG before any launch
+    (ADVICE r1), instead of overflowing the counters and hanging."""
+    w = wl.kepler_ensemble(batch=131072, nsteps=1)
+    with irk.Integrator(w.problem, w.dim, w.h, 2 ** 31 + 7, w.batch, w.params, balance=1) as ig:
+        Y = torch.tensor(w.y, dtype=torch.float64, device="cuda")
+        with pytest.raises(irk.IrkError) as ei:
+            ig.integrate(Y, ig.new_workspace())
+        assert ei.value.code == irk.E_ARG
+        assert np.array_equal(Y.cpu().numpy(), w.y)
