@@ -235,7 +235,8 @@ int run_chunks(irk_ctx *c, EnsArgs &a, char *ws, int64_t nblocks, int wpb, int s
             a.nslots = c->batch;
         } else {  // sort by the previous chunk's sweeps per step, deal warps to blocks
             const unsigned sb = (unsigned)((c->batch + 255) / 256 < 1184 ? (c->batch + 255) / 256 : 1184);
-            cudaMemsetAsync(sc.bins, 0, sizeof(int32_t) * irk::kCostBins, st);
+            const int rcm = cuda_check(c, cudaMemsetAsync(sc.bins, 0, sizeof(int32_t) * irk::kCostBins, st), "memset bins");
+            if (rcm) return rcm;
             irk::cost_hist_kernel<<<sb, 256, 0, st>>>(sc.csweeps, c->batch, prev_steps, sc.bins);
             irk::cost_scan_kernel<<<1, irk::kCostBins, 0, st>>>(sc.bins);
             irk::cost_scatter_kernel<<<sb, 256, 0, st>>>(sc.csweeps, c->batch, prev_steps, sc.bins, sc.sorted);
@@ -360,8 +361,11 @@ int launch_direct(irk_ctx *c, double *y, double t0, char *ws, double *energy, in
     const int64_t E = c->energy_every;
     auto sample = [&](int64_t idx) -> int {
         NvtxRange range("irk:energy_sample");
-        for (int t = 0; t < nlocal; ++t)
-            cudaMemcpyAsync(Qall + 3 * A[t].b0, A[t].yq, sizeof(double) * dl, cudaMemcpyDeviceToDevice, st);
+        for (int t = 0; t < nlocal; ++t) {
+            const int r = cuda_check(c, cudaMemcpyAsync(Qall + 3 * A[t].b0, A[t].yq, sizeof(double) * dl,
+                                                        cudaMemcpyDeviceToDevice, st), "energy sample: positions");
+            if (r) return r;
+        }
         if (nccl) {
             int r = nccl_allgather_inplace(c, Qall, (size_t)dl, st);
             if (r) return r;
@@ -383,7 +387,7 @@ int launch_direct(irk_ctx *c, double *y, double t0, char *ws, double *energy, in
         return rc;
     if ((rc = cuda_check(c, cudaStreamSynchronize(st), "sync"))) return rc;
     if (bad0 > 0 || c->nsteps == 0) {
-        if (iters) cudaMemsetAsync(iters, 0, sizeof(int64_t), st);
+        if (iters && (rc = cuda_check(c, cudaMemsetAsync(iters, 0, sizeof(int64_t), st), "memset iters"))) return rc;
         return cuda_check(c, cudaGetLastError(), "direct: frozen");
     }
     for (int t = 0; t < nlocal; ++t) irk::nbd_init_kernel<<<cb, 128, 0, st>>>(A[t]);
@@ -477,10 +481,12 @@ int launch_direct(irk_ctx *c, double *y, double t0, char *ws, double *energy, in
             const int64_t target = (E > 0 && energy) ? ((n / E + 1) * E < c->nsteps ? (n / E + 1) * E : c->nsteps)
                                                      : c->nsteps;
             c->h_ctl->target = target;
-            cudaMemcpyAsync(&ctl->target, &c->h_ctl->target, sizeof(int64_t), cudaMemcpyHostToDevice, st);
-            cudaGraphLaunch(gexec, st);
-            cudaMemcpyAsync(c->h_ctl, ctl, offsetof(irk::NbdCtl, target), cudaMemcpyDeviceToHost, st);
-            if ((rc = cuda_check(c, cudaStreamSynchronize(st), "direct device loop"))) {
+            if ((rc = cuda_check(c, cudaMemcpyAsync(&ctl->target, &c->h_ctl->target, sizeof(int64_t),
+                                                    cudaMemcpyHostToDevice, st), "H2D loop target")) ||
+                (rc = cuda_check(c, cudaGraphLaunch(gexec, st), "device loop graph launch")) ||
+                (rc = cuda_check(c, cudaMemcpyAsync(c->h_ctl, ctl, offsetof(irk::NbdCtl, target), cudaMemcpyDeviceToHost, st),
+                                 "D2H loop control")) ||
+                (rc = cuda_check(c, cudaStreamSynchronize(st), "direct device loop"))) {
                 cudaGraphExecDestroy(gexec);
                 return rc;
             }
@@ -496,7 +502,9 @@ int launch_direct(irk_ctx *c, double *y, double t0, char *ws, double *energy, in
         while (n < c->nsteps) {
             NvtxRange range("irk:host_loop_sweep");
             if ((rc = enqueue_sweep(st, 0, 0))) return rc;
-            cudaMemcpyAsync(c->h_ctl, ctl, sizeof(irk::NbdCtl), cudaMemcpyDeviceToHost, st);
+            if ((rc = cuda_check(c, cudaMemcpyAsync(c->h_ctl, ctl, sizeof(irk::NbdCtl), cudaMemcpyDeviceToHost, st),
+                                 "D2H sweep control")))
+                return rc;
             if ((rc = cuda_check(c, cudaStreamSynchronize(st), "direct sweep"))) return rc;
             if (c->h_ctl->halt) break;
             if (c->h_ctl->fin) {
@@ -509,7 +517,9 @@ int launch_direct(irk_ctx *c, double *y, double t0, char *ws, double *energy, in
     // final exchange: a divergence at the call's last step is recorded on every rank
     if (fused) {
         irk::nbd_xfinal_kernel<<<1, 1, 0, st>>>(A[0], n_done, stats);
-        cudaMemcpyAsync(c->h_ctl, ctl, sizeof(irk::NbdCtl), cudaMemcpyDeviceToHost, st);
+        if ((rc = cuda_check(c, cudaMemcpyAsync(c->h_ctl, ctl, sizeof(irk::NbdCtl), cudaMemcpyDeviceToHost, st),
+                             "D2H final control")))
+            return rc;
         if ((rc = cuda_check(c, cudaStreamSynchronize(st), "fused exchange final barrier"))) return rc;
         if (c->h_ctl->xerr)
             return fail(c, IRK_E_COMM, "fused exchange: a peer did not arrive within %d s", 60);
@@ -517,7 +527,9 @@ int launch_direct(irk_ctx *c, double *y, double t0, char *ws, double *energy, in
         if (nccl && (rc = nccl_allgather_inplace(c, Qg, (size_t)stride, st))) return rc;
         irk::nbd_final_kernel<<<1, 1, 0, st>>>(A[0], n_done, stats);
     }
-    if (iters) cudaMemcpyAsync(iters, &ctl->sweeps, sizeof(int64_t), cudaMemcpyDeviceToDevice, st);
+    if (iters && (rc = cuda_check(c, cudaMemcpyAsync(iters, &ctl->sweeps, sizeof(int64_t), cudaMemcpyDeviceToDevice, st),
+                                  "sweeps -> iters")))
+        return rc;
     return cuda_check(c, cudaGetLastError(), "direct launch");
 }
 
@@ -1262,9 +1274,12 @@ int irk_energy(irk_ctx *c, const double *y, double *H, void *stream) {
         if (!c->d_rows && (rc = cuda_check(c, cudaMalloc(&c->d_rows, sizeof(double) * 5 * N), "cudaMalloc energy")))
             return rc;
         double *Qall = c->d_rows, *terms = c->d_rows + 3 * N;
-        cudaMemcpyAsync(c->d_mass, c->params.data() + 2, sizeof(double) * N, cudaMemcpyHostToDevice, st);
         const int64_t b0 = (int64_t)c->rank * nloc;
-        cudaMemcpyAsync(Qall + 3 * b0, y, sizeof(double) * 3 * nloc, cudaMemcpyDeviceToDevice, st);
+        if ((rc = cuda_check(c, cudaMemcpyAsync(c->d_mass, c->params.data() + 2, sizeof(double) * N,
+                                                cudaMemcpyHostToDevice, st), "H2D mass")) ||
+            (rc = cuda_check(c, cudaMemcpyAsync(Qall + 3 * b0, y, sizeof(double) * 3 * nloc, cudaMemcpyDeviceToDevice, st),
+                             "energy: positions")))
+            return rc;
         if (c->nccl_comm && (rc = nccl_allgather_inplace(c, Qall, (size_t)(3 * nloc), st))) return rc;
         const double *v = y + (c->nccl_comm ? 3 * nloc : 3 * N);
         irk::nbd_energy_terms_kernel<<<(unsigned)((nloc + 127) / 128), 128, 0, st>>>(
