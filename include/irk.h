@@ -45,9 +45,9 @@ typedef struct irk_ctx irk_ctx; /* opaque, owned by the library */
 /* Problems (right-hand sides g(q,t) of q' = v, v' = g(q,t), Eq. ivp2). */
 enum irk_problem {
     IRK_KEPLER = 1,        /* planar Kepler, dim = 4; params {GM}                           */
-    IRK_NBODY = 2,         /* N-body Eq. Ham2, symmetric pairs, dim = 6N, N >= 2;
+    IRK_NBODY = 2,         /* N-body Eq. Ham2, cyclic pair order, dim = 6N, 2 <= N <= 8;
                               params {G, eps, m_1..m_N}                                   */
-    IRK_FPU_BETA = 3,      /* FPU-beta chain, fixed ends, dim = 2N; params {beta}            */
+    IRK_FPU_BETA = 3,      /* FPU-beta chain, fixed ends, dim = 2N, N in {32, 64, 96, 128}; params {beta} */
     IRK_HENON_HEILES = 4,  /* Listing 2, dim = 4; params {lambda, xi}          */
     IRK_NBODY_DIRECT = 5,  /* large-N direct sum, canonical blocked j-order, dim = 6N;
                               params {G, eps > 0, m_1..m_N}; batch must be 1                */

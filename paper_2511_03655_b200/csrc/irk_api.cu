@@ -814,9 +814,10 @@ int launch_chain(irk_ctx *c, double *y, double t0, char *ws, double *energy, int
     switch (c->dim / 2) {
     case 32: return launch_chain_t<1>(c, y, t0, ws, energy, iters, st);
     case 64: return launch_chain_t<2>(c, y, t0, ws, energy, iters, st);
+    case 96: return launch_chain_t<3>(c, y, t0, ws, energy, iters, st);
     case 128: return launch_chain_t<4>(c, y, t0, ws, energy, iters, st);
     }
-    return fail(c, IRK_E_ARG, "irk_integrate: IRK_FPU_BETA supports N in {32, 64, 128} sites");
+    return fail(c, IRK_E_ARG, "irk_integrate: IRK_FPU_BETA supports N in {32, 64, 96, 128} sites");
 }
 
 int launch_nbody(irk_ctx *c, double *y, double t0, char *ws, double *energy, int64_t *iters, cudaStream_t st) {
@@ -826,9 +827,10 @@ int launch_nbody(irk_ctx *c, double *y, double t0, char *ws, double *energy, int
     case 4: return launch_nbody_t<4>(c, y, t0, ws, energy, iters, st);
     case 5: return launch_nbody_t<5>(c, y, t0, ws, energy, iters, st);
     case 6: return launch_nbody_t<6>(c, y, t0, ws, energy, iters, st);
+    case 7: return launch_nbody_t<7>(c, y, t0, ws, energy, iters, st);
     case 8: return launch_nbody_t<8>(c, y, t0, ws, energy, iters, st);
     }
-    return fail(c, IRK_E_ARG, "irk_integrate: IRK_NBODY ensembles support N in {2,3,4,5,6,8} bodies");
+    return fail(c, IRK_E_ARG, "irk_integrate: IRK_NBODY ensembles support N in {2,...,8} bodies");
 }
 
 template <int N>
@@ -1006,13 +1008,13 @@ irk_ctx *irk_create(int problem, int dim, double h, int64_t nsteps, int64_t batc
         break;
     case IRK_FPU_BETA:
         if (dim < 2 || dim % 2) return bad("irk_create: FPU needs an even dim >= 2");
-        if (dim / 2 != 32 && dim / 2 != 64 && dim / 2 != 128)
-            return bad("irk_create: IRK_FPU_BETA supports N in {32, 64, 128} sites (one warp per chain)");
+        if (dim / 2 != 32 && dim / 2 != 64 && dim / 2 != 96 && dim / 2 != 128)
+            return bad("irk_create: IRK_FPU_BETA supports N in {32, 64, 96, 128} sites (one warp per chain)");
         break;
     case IRK_NBODY: {
         if (dim % 6 || dim < 12) return bad("irk_create: N-body needs dim = 6N, N >= 2");
         const int N = dim / 6;
-        if (N > 6 && N != 8) return bad("irk_create: IRK_NBODY ensembles support N in {2,...,6, 8}");
+        if (N > 8) return bad("irk_create: IRK_NBODY ensembles support N in {2,...,8}");
         break;
     }
     case IRK_NBODY_DIRECT:
@@ -1293,6 +1295,7 @@ int irk_energy(irk_ctx *c, const double *y, double *H, void *stream) {
         switch (c->dim / 2) {
         case 32: energy_fpu_kernel<32><<<nb, 128, 0, st>>>(y, H, c->batch, c->params[0]); break;
         case 64: energy_fpu_kernel<64><<<nb, 128, 0, st>>>(y, H, c->batch, c->params[0]); break;
+        case 96: energy_fpu_kernel<96><<<nb, 128, 0, st>>>(y, H, c->batch, c->params[0]); break;
         case 128: energy_fpu_kernel<128><<<nb, 128, 0, st>>>(y, H, c->batch, c->params[0]); break;
         default: return fail(c, IRK_E_ARG, "irk_energy: unsupported N");
         }
@@ -1305,6 +1308,7 @@ int irk_energy(irk_ctx *c, const double *y, double *H, void *stream) {
         case 4: launch_energy_nbody_t<4>(c, y, H, st); break;
         case 5: launch_energy_nbody_t<5>(c, y, H, st); break;
         case 6: launch_energy_nbody_t<6>(c, y, H, st); break;
+        case 7: launch_energy_nbody_t<7>(c, y, H, st); break;
         case 8: launch_energy_nbody_t<8>(c, y, H, st); break;
         default: return fail(c, IRK_E_ARG, "irk_energy: unsupported N");
         }

@@ -494,10 +494,10 @@ def test_config3_full_batch_sampled(irk, orc):
 
 @pytest.mark.parametrize("mapping", [1, 8])
 def test_nbody_small_n_variants(irk, orc, mapping):
-    """Other N of both N-body mappings (N = 2, 3, 4, 5, 8; body per lane and
+    """Other N of both N-body mappings (N = 2, 3, 4, 5, 7, 8; body per lane and
     stage per lane): random softened systems, bitwise."""
     rng = np.random.default_rng(3)
-    for N in (2, 3, 4, 5, 8):
+    for N in (2, 3, 4, 5, 7, 8):
         B = 23
         q = rng.standard_normal((3 * N, B))
         v = 0.3 * rng.standard_normal((3 * N, B))
@@ -545,16 +545,17 @@ def test_config4_full_batch_sampled(irk, orc):
 
 
 def test_fpu_other_sizes_and_energy_entry(irk, orc):
-    for N in (32, 128):
+    for N in (32, 96, 128):
         w = wl.fpu_ensemble(batch=5, nsteps=500, N=N)
         g = run_gpu(irk, w, energy_every=100)
         o = orc.integrate(w.problem, w.y, w.params, w.h, w.nsteps, energy_every=100)
         assert_parity(g, o, energy=True)
-    w = wl.fpu_ensemble(batch=33)
-    with irk.Integrator(w.problem, w.dim, w.h, 1, w.batch, w.params) as ig:
-        H = ig.energy(torch.tensor(w.y, device="cuda")).cpu().numpy()
-    Ho = np.array([orc.energy(w.problem, w.dim, w.params, w.y[:, b]) for b in range(w.batch)])
-    assert np.array_equal(H, Ho)
+    for N in (64, 96):
+        w = wl.fpu_ensemble(batch=33, N=N)
+        with irk.Integrator(w.problem, w.dim, w.h, 1, w.batch, w.params) as ig:
+            H = ig.energy(torch.tensor(w.y, device="cuda")).cpu().numpy()
+        Ho = np.array([orc.energy(w.problem, w.dim, w.params, w.y[:, b]) for b in range(w.batch)])
+        assert np.array_equal(H, Ho)
 
 
 # ------------------------------------------------------------------ config 5

@@ -64,9 +64,10 @@ def test_library_tableau_bitwise_equals_oracle_and_mpmath(irk, orc):
     (1, 4, 0.1, 10, 2**31),      # batch > 2^31 - 1 (int32 trajectory indices)
     (9, 4, 0.1, 10, 4),          # unknown problem
     (2, 13, 0.1, 10, 4),         # N-body dim % 6
-    (2, 42, 0.1, 10, 4),         # N-body ensembles: N = 7 unsupported
+    (2, 54, 0.1, 10, 4),         # N-body ensembles: N = 9 unsupported (2 <= N <= 8)
     (3, 7, 0.1, 10, 4),          # FPU odd dim
-    (3, 40, 0.1, 10, 4),         # FPU: N must be 32, 64 or 128 (one warp per chain)
+    (3, 40, 0.1, 10, 4),         # FPU: N must be 32, 64, 96 or 128 (one warp per chain)
+    (3, 160, 0.1, 10, 4),        # FPU: N = 80 unsupported
 ])
 def test_create_argument_errors(irk, args):
     with pytest.raises(irk.IrkError):
