@@ -29,9 +29,6 @@ namespace irk {
 #define G1_BLOCK 64
 #endif
 constexpr int G1_THREADS = G1_BLOCK;
-#ifndef G1Q_PARK
-#define G1Q_PARK 0  // 1: park a blocked unit for its predecessor's lane (measured 92 -> 120 ms: the counter runs ahead)
-#endif
 #ifndef G1Q_QREG
 #define G1Q_QREG 1  // the heavy ens_g1q keeps the stage positions in registers
 #endif
@@ -411,23 +408,8 @@ __global__ void __maxnreg__(MAXREG) ens_g1q_kernel(const __grid_constant__ EnsAr
 #endif
             }
             if (c > 0 && ld_acquire(&qa.progress[bb]) < c) {  // predecessor unit still running
-#if G1Q_PARK
-                // park the unit for the lane finishing (bb, c - 1) and fetch another one
-                // (hand-off protocol of ens_common.cuh: exactly one of the two runs it)
-                if (atomicCAS(&qa.orphan[bb], 0, (int)c) == 0) {
-                    __threadfence();
-                    if (!(ld_acquire(&qa.progress[bb]) >= c && atomicCAS(&qa.orphan[bb], (int)c, 0) == (int)c)) {
-                        u = -1;
-                        continue;
-                    }
-                } else {  // another unit of bb is parked already (rare): wait
-                    __nanosleep(1024);
-                    continue;
-                }
-#else
                 __nanosleep(1024);
                 continue;
-#endif
             }
 #ifdef IRK_TRACE
             t_start = irk_now();
@@ -613,34 +595,8 @@ __global__ void __maxnreg__(MAXREG) ens_g1q_kernel(const __grid_constant__ EnsAr
 #ifdef IRK_TRACE
                 irk_trace_unit(c, b, t_fetch, t_start, sweeps);
 #endif
-#if G1Q_PARK
-                // the next unit of this trajectory was parked for this lane: continue it
-                // from the registers (same arithmetic as reloading the stored state)
-                bool carry = false;
-                while (claim_orphan(qa, b, c + 1)) {
-                    ++c;
-                    if (finite) {
-                        carry = true;
-                        break;
-                    }
-                    st_release(&qa.progress[b], (int32_t)(c + 1));  // frozen trajectory: nothing to do
-                }
-                if (carry) {
-                    const int64_t c0 = c * qa.qchunk;
-                    len = (a.nsteps - c0 < qa.qchunk) ? a.nsteps - c0 : qa.qchunk;
-                    n = hits = sweeps = 0;
-                    dhmax = 0.0;
-#ifdef IRK_TRACE
-                    t_fetch = t_start = irk_now();
-#endif
-                } else {
-                    b = -1;
-                    continue;
-                }
-#else
                 b = -1;
                 continue;
-#endif
             }
         }
         // a4 (second half) / next step's a1: V_i = v + D(W_i., Lv), W = fin ? nu : mu
