@@ -76,7 +76,9 @@ enum irk_option {
                                  2 / 4 lanes per trajectory (4 / 2 stages per lane), IRK_MAP_G8 = 8 lanes per
                                  trajectory, one stage per lane (warp-shuffle contractions and
                                  convergence reduction).  IRK_NBODY: IRK_MAP_G1 = body per lane,
-                                 IRK_MAP_G8 = stage per lane (shared-memory all-gather).  Auto
+                                 IRK_MAP_G8 = stage per lane (shared-memory all-gather),
+                                 IRK_MAP_G8M = stage per lane with the two stage contractions on
+                                 the FP64 tensor core (DMMA, fragments by warp shuffle).  Auto
                                  picks by problem, N and batch size from measured crossovers
                                  ("ens_gs" and "ens_nbody8"; the chunked IRK_OPT_SCHEDULE = 1 keeps
                                  body per lane).  Bitwise-neutral.  */
@@ -110,7 +112,7 @@ enum irk_option {
                                  irk_local_energy_error (ensemble problems only)                   */
 };
 
-enum irk_mapping { IRK_MAP_AUTO = 0, IRK_MAP_G1 = 1, IRK_MAP_G2 = 2, IRK_MAP_G4 = 4, IRK_MAP_G8 = 8 };
+enum irk_mapping { IRK_MAP_AUTO = 0, IRK_MAP_G1 = 1, IRK_MAP_G2 = 2, IRK_MAP_G4 = 4, IRK_MAP_G8 = 8, IRK_MAP_G8M = 9 };
 
 /* Create a context for `batch` independent trajectories of `problem` in
  * dimension `dim`, step h (finite, != 0; negative allowed), nsteps >= 0 steps per

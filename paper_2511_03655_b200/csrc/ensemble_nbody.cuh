@@ -43,8 +43,7 @@ constexpr int NB_THREADS = 64;
 // Hamiltonian of one system from shared memory (canonical term order, Neumaier;
 // oracle energy_nbody): kinetic terms i = 0..N-1, then row sums over j > i.
 template <int NB>
-__device__ double nbody_energy(const double *qv, const NBodyParams &P) {
-    const double *q = qv, *v = qv + 3 * NB;
+__device__ double nbody_energy(const double *q, const double *v, const NBodyParams &P) {
     Neumaier tot;
     for (int i = 0; i < NB; ++i) {
         double k = dfma(v[3 * i + 2], v[3 * i + 2], dfma(v[3 * i + 1], v[3 * i + 1], dmul(v[3 * i], v[3 * i])));
@@ -62,6 +61,10 @@ __device__ double nbody_energy(const double *qv, const NBodyParams &P) {
         tot.add(row.result());
     }
     return tot.result();
+}
+template <int NB>
+__device__ double nbody_energy(const double *qv, const NBodyParams &P) {
+    return nbody_energy<NB>(qv, qv + 3 * NB, P);
 }
 
 // Acceleration of body `body` at one stage (canonical RHS, see the header).

@@ -27,6 +27,7 @@
 #include "ensemble_fo.cuh"
 #include "ensemble_nbody.cuh"
 #include "ensemble_nbody8.cuh"
+#include "ensemble_nbody8m.cuh"
 #include "ensemble_chain.cuh"
 #include "nbody_direct.cuh"
 #include "problems.cuh"
@@ -52,6 +53,7 @@ struct irk_ctx {
     int nbody_blocks_per_sm[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
     int fo_blocks_per_sm = 0;
     int nbody8_blocks_per_sm[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+    int nbody8m_blocks_per_sm[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
     int local_energy = 0;  // IRK_OPT_LOCAL_ENERGY
     int64_t energy_every = 0;
     Tableau T;
@@ -743,7 +745,22 @@ int launch_nbody_t(irk_ctx *c, double *y, double t0, char *ws, double *energy, i
     // chunked schedule (IRK_OPT_SCHEDULE = 1) keeps body-per-lane
     const bool stage_per_lane =
         c->mapping == IRK_MAP_G8 || (c->mapping == IRK_MAP_AUTO && c->schedule != 1 && nbody8_auto(NB, c->batch));
-    c->mapping_used = stage_per_lane ? IRK_MAP_G8 : IRK_MAP_G1;
+    const bool dmma = c->mapping == IRK_MAP_G8M;
+    c->mapping_used = dmma ? IRK_MAP_G8M : stage_per_lane ? IRK_MAP_G8 : IRK_MAP_G1;
+    if (dmma) {
+        constexpr int SPB = irk::N8M_THREADS / 32 * 4;  // trajectories per block
+        return (IRK_UNIT_G && P.G == 1.0)
+                   ? launch_queue(c, irk::ens_nbody8m_kernel<NB, true>, irk::N8M_THREADS, SPB,
+                                  &c->nbody8m_blocks_per_sm[NB], a, ws, st,
+                                  [&](const EnsArgs &aa, const irk::QueueArgs &qa, unsigned nb) {
+                                      irk::ens_nbody8m_kernel<NB, true><<<nb, irk::N8M_THREADS, 0, st>>>(aa, qa, P);
+                                  })
+                   : launch_queue(c, irk::ens_nbody8m_kernel<NB, false>, irk::N8M_THREADS, SPB,
+                                  &c->nbody8m_blocks_per_sm[NB], a, ws, st,
+                                  [&](const EnsArgs &aa, const irk::QueueArgs &qa, unsigned nb) {
+                                      irk::ens_nbody8m_kernel<NB, false><<<nb, irk::N8M_THREADS, 0, st>>>(aa, qa, P);
+                                  });
+    }
     if (stage_per_lane)
         return (IRK_UNIT_G && P.G == 1.0)
                    ? launch_queue(c, irk::ens_nbody8_kernel<NB, true>, irk::N8_THREADS, irk::N8_THREADS / 8,
@@ -1104,8 +1121,12 @@ int irk_set_option(irk_ctx *c, int key, int64_t val) {
         c->schedule = (int)val;
         return IRK_OK;
     case IRK_OPT_MAPPING:
-        if (val != IRK_MAP_AUTO && val != IRK_MAP_G1 && val != IRK_MAP_G2 && val != IRK_MAP_G4 && val != IRK_MAP_G8)
-            return fail(c, IRK_E_ARG, "irk_set_option: MAPPING must be 0 (auto), 1 (g1), 2 (g2), 4 (g4) or 8 (g8)");
+        if (val != IRK_MAP_AUTO && val != IRK_MAP_G1 && val != IRK_MAP_G2 && val != IRK_MAP_G4 && val != IRK_MAP_G8 &&
+            val != IRK_MAP_G8M)
+            return fail(c, IRK_E_ARG,
+                        "irk_set_option: MAPPING must be 0 (auto), 1 (g1), 2 (g2), 4 (g4), 8 (g8) or 9 (g8m)");
+        if (val == IRK_MAP_G8M && c->problem != IRK_NBODY)
+            return fail(c, IRK_E_ARG, "irk_set_option: the g8m mapping is built for the N-body ensembles");
         if ((val == IRK_MAP_G4 || val == IRK_MAP_G2) && c->problem != IRK_KEPLER && c->problem != IRK_HENON_HEILES)
             return fail(c, IRK_E_ARG, "irk_set_option: the g2 / g4 mappings are built for Kepler and Henon-Heiles");
         if (val == IRK_MAP_G8 && c->problem != IRK_KEPLER && c->problem != IRK_HENON_HEILES && c->problem != IRK_NBODY &&
@@ -1429,3 +1450,4 @@ extern "C" int irk_trace_set(void *buf, int64_t cap) {
     return cudaMemcpyToSymbol(irk::g_irk_trace_cap, &c, sizeof c) == cudaSuccess ? 0 : -1;
 }
 #endif
+

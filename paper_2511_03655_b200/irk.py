@@ -17,7 +17,7 @@ OK, W_MAXITER, E_ARG, E_CUDA, E_DIVERGED, E_COMM, E_STATE = 0, 1, -1, -2, -3, -4
 OPT_MODE, OPT_MAX_ITERS, OPT_ENERGY_EVERY, OPT_MAPPING, OPT_BALANCE, OPT_VSHARDS = 1, 2, 3, 4, 5, 6
 OPT_LOCAL_ENERGY = 7
 OPT_SCHEDULE = 8
-MAP_AUTO, MAP_G1, MAP_G2, MAP_G4, MAP_G8 = 0, 1, 2, 4, 8  # IRK_OPT_MAPPING (include/irk.h)
+MAP_AUTO, MAP_G1, MAP_G2, MAP_G4, MAP_G8, MAP_G8M = 0, 1, 2, 4, 8, 9  # IRK_OPT_MAPPING (include/irk.h)
 OPT_DEVICE_LOOP = 9
 OPT_EXCHANGE = 10  # IRK_NBODY_DIRECT under set_comm: 0 = ncclAllGather, 1 = fused NVLink stores
 EXCHANGE_ALLGATHER, EXCHANGE_FUSED = 0, 1

@@ -1,9 +1,9 @@
 """N-body ensembles, every supported N: body-per-lane (IRK_OPT_MAPPING = 1) vs
-stage-per-lane (8) -- time per call (CUDA events, best of 3) and bitwise
-agreement.  N = 6 uses the config-3 generator; other N seeded random softened
+stage-per-lane (8) vs stage-per-lane with DMMA contractions (9) -- time per call
+(CUDA events, best of 3) and bitwise agreement.  N = 6 uses the config-3 generator; other N seeded random softened
 systems (as tests/test_gpu_parity.py::test_nbody_small_n_variants).
 
-python tools/nb_map_ab.py [--nsteps 1000] [--batches 2048,16384] [--out f.json]
+python tools/nb_map_ab.py [--nsteps 1000] [--batches 2048,16384] [--ns 2,3,4,5,6,8] [--out f.json]
 """
 import argparse
 import json
@@ -50,16 +50,19 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--nsteps", type=int, default=1000)
     ap.add_argument("--batches", default="2048,16384")
+    ap.add_argument("--ns", default="2,3,4,5,6,8")
     ap.add_argument("--out", default="")
     a = ap.parse_args()
     res = []
-    for N in (2, 3, 4, 5, 6, 8):
+    for N in [int(x) for x in a.ns.split(",")]:
         for B in [int(x) for x in a.batches.split(",")]:
             w = system(N, B, a.nsteps)
             t1, y1 = run(w, irk.MAP_G1)
             t8, y8 = run(w, irk.MAP_G8)
-            r = dict(N=N, batch=B, nsteps=a.nsteps, body_per_lane_ms=t1, stage_per_lane_ms=t8,
-                     bitwise_equal=bool(np.array_equal(y1, y8, equal_nan=True)))
+            t9, y9 = run(w, irk.MAP_G8M)
+            r = dict(N=N, batch=B, nsteps=a.nsteps, body_per_lane_ms=t1, stage_per_lane_ms=t8, dmma_ms=t9,
+                     bitwise_equal=bool(np.array_equal(y1, y8, equal_nan=True)),
+                     dmma_bitwise_equal=bool(np.array_equal(y1, y9, equal_nan=True)))
             print(json.dumps(r), flush=True)
             res.append(r)
     if a.out:
