@@ -33,9 +33,9 @@
 //   a5  Delta_l = max_s |Q_s,l - Q_s,l^old|: a reduce-scatter of the 8 stage lanes of
 //       a trajectory (xor 16, 8, 4: each lane ends owning <= 3 components, their
 //       stop-test state m, p in registers), R2 test, ballot over the trajectory's lanes
-//   a6  fin: S(Lq), S(Lv) = the same fragments against a coefficient matrix of ones
-//       (DMMA: fma(1, x, acc) = acc + x, the canonical dadd chain in stage order);
-//       the owners of components update q, v in shared memory   Eq. yn3
+//   a6  fin: the owner of component l (lane s = l mod 8 of the trajectory) sums
+//       column l of the Lq / Lv tile in stage order and updates q, v in shared
+//       memory                                                    Eq. yn3
 //   a3  F_s = accelerations at stage s (n8_accel, cyclic partner order R-8)
 //   a4  D = W Lv, W = nu~ for a finished step (next step's nu-init), else mu~;
 //       V = v + D; the next sweep's Lq = hb_s V                Eq. IRK_FP2 l.4-5
@@ -91,21 +91,26 @@ __device__ __noinline__ double n8m_energy(const double *q, const double *v, cons
     return nbody_energy<NB>(q, v, P);
 }
 
-// a6 for the components l = s mod 8 of the lane: y_l += S_l (S from the ones
-// contraction, every stage lane holds all of its trajectory's sums)
-template <int d, int T>
-__device__ __forceinline__ void n8m_owner_update(double *y, const double *S, int s, bool &finite) {
+// a6 for the components l = s + 8 i of the lane: y_l += S(column l of the stage
+// tile), the canonical dadd chain over stages 0..7 (oracle update order); the
+// finiteness of the result as a running max of exponent fields (integer pipe)
+template <int d, int NO, class Tile>
+__device__ __forceinline__ void n8m_owner_update(double *y, const double *X, int g, int s, unsigned &expmax) {
 #pragma unroll
-    for (int l = 0; l < d; ++l)
-        if ((l & 7) == s) {
-            y[l] = dadd(y[l], S[l]);
-            finite = finite && isfinite(y[l]);
+    for (int i = 0; i < NO; ++i) {
+        const int l = s + 8 * i;
+        if (l < d) {
+            double sum = X[Tile::row(g, 0) + l];
+#pragma unroll
+            for (int j = 1; j < 8; ++j) sum = dadd(sum, X[Tile::row(g, j) + l]);
+            const double yn = dadd(y[l], sum);
+            y[l] = yn;
+            const unsigned ex = (unsigned)__double2hiint(yn) & 0x7ff00000u;
+            expmax = ex > expmax ? ex : expmax;
         }
+    }
 }
 
-// D[2t], D[2t+1] = sum_j A[s][j] B_t[j][.] for every tile t: the first k halves of
-// all tiles, then the second halves (volatile asm keeps this order, so the nine
-// independent chains overlap the DMMA latency)
 // B fragments of every tile from the stage tile (both k halves)
 template <int T>
 __device__ __forceinline__ void n8m_frags(const double *X, int fb0, int fb1, double *b0, double *b1) {
@@ -277,17 +282,9 @@ __global__ void __maxnreg__(N8M_MAXREG) ens_nbody8m_kernel(const __grid_constant
         const bool fin = live && (stop || k >= a.max_iters);
         const unsigned finmask = __ballot_sync(FULL, fin), livemask = __ballot_sync(FULL, live);
         const bool anyfin = finmask != 0u, allfin = (finmask & livemask) == livemask;
-        // ---- a6 (positions): q += S(Lq) (ones x the Lq fragments), component owners ----
-        bool finite = true;
-        if (anyfin) {  // (mma.sync.aligned: every DMMA group runs converged, its owner updates after it)
-            double S[d2];
-            {
-                double b0[T], b1[T];
-                n8m_frags<T>(X, fb0, fb1, b0, b1);
-                n8m_contract<T>(S, 1.0, 1.0, b0, b1);
-            }
-            if (fin) n8m_owner_update<d, T>(qv, S, s, finite);
-        }
+        // ---- a6 (positions): q += S(Lq) by the component owners, from the Lq tile ----
+        unsigned expmax = 0;  // non-finite result <=> an exponent field of all ones
+        if (fin) n8m_owner_update<d, NO, Tile>(qv, X, g, s, expmax);
         // ---- a3: F_s ; Lv_s = hb_s F_s -> own row ----
         {
             double F[d], Qs[d];
@@ -310,17 +307,11 @@ __global__ void __maxnreg__(N8M_MAXREG) ens_nbody8m_kernel(const __grid_constant
                     make_double2(dmul(hb_s, F[2 * t]), (2 * t + 1 < d) ? dmul(hb_s, F[2 * t + 1]) : 0.0);
         }
         __syncwarp();  // Lv rows written
-        // ---- a4: D = W Lv (W per trajectory) ; a6 (velocities) v += S(Lv) ----
+        // ---- a4: D = W Lv (W per trajectory) ----
         double Dv[d2];
         {
             double b0[T], b1[T];
             n8m_frags<T>(X, fb0, fb1, b0, b1);
-            if (anyfin) {
-                double S[d2];
-                n8m_contract<T>(S, 1.0, 1.0, b0, b1);
-                if (fin) n8m_owner_update<d, T>(qv + VO, S, s, finite);
-                __syncwarp();
-            }
             // one pass with the slot's common W; a second (nu~) pass if the slot's
             // live trajectories disagree
             const bool nu = anyfin && allfin;
@@ -333,7 +324,8 @@ __global__ void __maxnreg__(N8M_MAXREG) ens_nbody8m_kernel(const __grid_constant
                 for (int l = 0; l < d2; ++l) Dv[l] = fin ? Dn[l] : Dv[l];
             }
         }
-        const unsigned nonfinite = __ballot_sync(FULL, !finite);  // (every lane votes: not under `fin &&`)
+        if (fin) n8m_owner_update<d, NO, Tile>(qv + VO, X, g, s, expmax);  // a6 (velocities) from the Lv tile
+        const unsigned nonfinite = __ballot_sync(FULL, expmax == 0x7ff00000u);  // (every lane votes)
         const bool bad = fin && ((nonfinite & gmask) != 0u);
         __syncwarp();  // v updated; every lane has read its Lv fragments
         if (fin) {
