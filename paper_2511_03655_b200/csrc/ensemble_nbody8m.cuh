@@ -58,6 +58,12 @@ constexpr int N8M_THREADS = 64;  // 2 warps = 2 slots = 8 trajectories per block
 #ifndef N8M_MAXREG
 #define N8M_MAXREG 168
 #endif
+#ifndef N8M_DREUSE
+#define N8M_DREUSE 1  // pair differences formed once per stage (n8m_accel)
+#endif
+#ifndef N8M_A2SYNC
+#define N8M_A2SYNC 0
+#endif
 #ifndef N8M_QSMEM
 #define N8M_QSMEM 1  // stage positions Q between sweeps in shared memory ([component][lane]), not registers
 #endif
@@ -108,6 +114,53 @@ __device__ __forceinline__ void n8m_owner_update(double *y, const double *X, int
             const unsigned ex = (unsigned)__double2hiint(yn) & 0x7ff00000u;
             expmax = ex > expmax ? ex : expmax;
         }
+    }
+}
+
+// Accelerations of all NB bodies at one stage (oracle accel_nbody_pairs, cyclic
+// partner order R-8), like n8_accel but each pair difference d = Q_j - Q_i (i < j)
+// formed once: body i adds fma(m_j w, d, a), body j adds fma(-(m_i w), d, a) --
+// Q_i - Q_j is exactly -d in round-to-nearest, and the negation is an operand
+// modifier -- 45 instead of 135 subtractions per stage for N = 6.
+template <int NB, bool G1>
+__device__ __forceinline__ void n8m_accel(const double *Q, double *A, const NBodyParams &P, const double *sm, bool &ok) {
+    constexpr int NP = NB * (NB - 1) / 2;
+    double w[NP], dx[NP], dy[NP], dz[NP];
+#pragma unroll
+    for (int i = 0; i < NB; ++i)
+#pragma unroll
+        for (int j = 0; j < NB; ++j) {
+            if (j <= i) continue;
+            const int p = i * NB - i * (i + 1) / 2 + (j - i - 1);
+            dx[p] = dsub(Q[3 * j], Q[3 * i]);
+            dy[p] = dsub(Q[3 * j + 1], Q[3 * i + 1]);
+            dz[p] = dsub(Q[3 * j + 2], Q[3 * i + 2]);
+            const double r2 = dfma(dz[p], dz[p], dfma(dy[p], dy[p], dfma(dx[p], dx[p], P.eps2)));
+            if (G1) {
+                bool unused = true;
+                ok = ok && weight_range_ok(r2);
+                w[p] = drcp_fast(dmul(r2, dsqrt_fast(r2, unused)), unused);
+            } else {
+                w[p] = ddiv_fast(P.G, dmul(r2, dsqrt_fast(r2, ok)), ok);
+            }
+        }
+#pragma unroll
+    for (int i = 0; i < NB; ++i) {
+        double ax = 0.0, ay = 0.0, az = 0.0;
+#pragma unroll
+        for (int delta = 1; delta < NB; ++delta) {
+            const int j = (i + delta) % NB;
+            const int lo = i < j ? i : j, hi = i < j ? j : i;
+            const int p = lo * NB - lo * (lo + 1) / 2 + (hi - lo - 1);
+            const double sw = dmul(sm[j], w[p]);
+            const double sg = i < j ? sw : -sw;  // (a sign flip: exact)
+            ax = dfma(sg, dx[p], ax);
+            ay = dfma(sg, dy[p], ay);
+            az = dfma(sg, dz[p], az);
+        }
+        A[3 * i] = ax;
+        A[3 * i + 1] = ay;
+        A[3 * i + 2] = az;
     }
 }
 
@@ -240,12 +293,19 @@ __global__ void __maxnreg__(N8M_MAXREG) ens_nbody8m_kernel(const __grid_constant
             }
         }
         if (live) ++k;
+        // the stop test runs from the second sweep of a step (Delta^[1] is not tested):
+        // sweeps where no trajectory of the slot tests skip the E tile
+        const bool k2 = live && k >= 2;
+        const bool anyk2 = __any_sync(FULL, k2);
         __syncwarp();  // Lq rows written
         // ---- a2: Q_s = q + D(mu_s., Lq) ; |Q_s - Q_s^old| -> own row of E ----
         {
             double b0[T], b1[T], Dq[d2];
             n8m_frags<T>(X, fb0, fb1, b0, b1);
             n8m_contract<T>(Dq, aM0, aM1, b0, b1);
+#if N8M_A2SYNC
+            __syncwarp();  // (a scheduling fence: the nine DMMA chains issue before their consumers)
+#endif
 #pragma unroll
             for (int t = 0; t < T; ++t) {
                 const double d0 = Dq[2 * t], d1 = Dq[2 * t + 1];
@@ -254,7 +314,7 @@ __global__ void __maxnreg__(N8M_MAXREG) ens_nbody8m_kernel(const __grid_constant
                 longlong2 e;
                 e.x = absdiff_bits(q0, N8M_Q(2 * t));
                 e.y = (2 * t + 1 < d) ? absdiff_bits(q1, N8M_Q(2 * t + 1)) : 0;
-                *reinterpret_cast<longlong2 *>(&E[myrow + 2 * t]) = e;
+                if (anyk2) *reinterpret_cast<longlong2 *>(&E[myrow + 2 * t]) = e;
                 N8M_Q(2 * t) = q0;
                 N8M_Q(2 * t + 1) = q1;
             }
@@ -263,11 +323,10 @@ __global__ void __maxnreg__(N8M_MAXREG) ens_nbody8m_kernel(const __grid_constant
         // ---- a5: Delta_l (NaN-ignoring max over the 8 stages) and reading R2 for the
         // owned components l = s + 8 i ----
         bool ok_lane = true;
-        const bool k2 = live && k >= 2;
 #pragma unroll
         for (int i = 0; i < NO; ++i) {
             const int l = s + 8 * i;
-            if (l < d) {
+            if (anyk2 && l < d) {
                 int64_t ev[8];
 #pragma unroll
                 for (int j = 0; j < 8; ++j) ev[j] = E[Tile::row(g, j) + l];
@@ -291,7 +350,11 @@ __global__ void __maxnreg__(N8M_MAXREG) ens_nbody8m_kernel(const __grid_constant
 #pragma unroll
             for (int l = 0; l < d; ++l) Qs[l] = N8M_Q(l);
             bool ok = true;
+#if N8M_DREUSE
+            n8m_accel<NB, G1>(Qs, F, P, sm, ok);
+#else
             n8_accel<NB, false, G1>(Qs, F, P, sm, ok);
+#endif
             if (!ok && live) {  // exact intrinsics, same bits (out of line, rare)
                 double row[d];
 #pragma unroll
