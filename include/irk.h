@@ -78,9 +78,9 @@ enum irk_option {
                                  convergence reduction).  IRK_NBODY: IRK_MAP_G1 = body per lane,
                                  IRK_MAP_G8 = stage per lane (shared-memory all-gather),
                                  IRK_MAP_G8M = stage per lane with the two stage contractions on
-                                 the FP64 tensor core (DMMA, fragments by warp shuffle).  Auto
+                                 the FP64 tensor core (DMMA m8n8k4; ensemble_nbody8m.cuh).  Auto
                                  picks by problem, N and batch size from measured crossovers
-                                 ("ens_gs" and "ens_nbody8"; the chunked IRK_OPT_SCHEDULE = 1 keeps
+                                 ("ens_gs", "ens_nbody8", "ens_nbody8m"; the chunked IRK_OPT_SCHEDULE = 1 keeps
                                  body per lane).  Bitwise-neutral.  */
     IRK_OPT_BALANCE = 5,      /* ensemble scheduling: -1 = auto (default), 0 = off, C > 0 = run the
                                  call in chunks of C steps, re-sorting trajectories by the cost of

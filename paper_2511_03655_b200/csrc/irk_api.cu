@@ -558,7 +558,7 @@ EnsArgs ens_args(irk_ctx *c, double *y, double t0, char *ws, double *energy, int
 // (one unit per trajectory when every trajectory has its own slot, else ~32).
 template <class KernelPtr, class LaunchFn>
 int launch_queue(irk_ctx *c, KernelPtr kernel, int threads, int spb, int *bps_cache, EnsArgs &a, char *ws,
-                 cudaStream_t st, LaunchFn launch, int units = 32, int max_bps = 0) {
+                 cudaStream_t st, LaunchFn launch, int units = 32, int max_bps = 0, int64_t unit_steps = 0) {
     int rc;
     if (!*bps_cache &&
         (rc = cuda_check(c, cudaOccupancyMaxActiveBlocksPerMultiprocessor(bps_cache, kernel, threads, 0), "occupancy")))
@@ -578,6 +578,7 @@ int launch_queue(irk_ctx *c, KernelPtr kernel, int threads, int spb, int *bps_ca
     qa.counter = reinterpret_cast<unsigned long long *>(sc.bins);
     int64_t chunk = c->nsteps;
     if (c->balance > 0) chunk = c->balance;
+    else if (c->balance < 0 && unit_steps > 0) chunk = unit_steps;
     else if (c->balance < 0 && c->batch > resident_blocks * spb) chunk = (c->nsteps + units - 1) / units;
     if (chunk < 1) chunk = 1;
     qa.qchunk = chunk;
@@ -656,17 +657,20 @@ int launch_gs(irk_ctx *c, const P &prob, EnsArgs &a, char *ws, cudaStream_t st) 
     return cuda_check(c, cudaGetLastError(), "advance_n launch");
 }
 
-// IRK_OPT_MAPPING auto for the N-body ensembles: stage per lane (ens_nbody8) where
-// tools/nb_map_ab.py measured it faster than body per lane (1,000 steps, batches
-// 2,048 / 6,144 / 16,384 / 65,536; profiles/r1/nb_map_ab.json): N = 3, 4, 6 at every
-// batch (config 3: 40.6 vs 45.8 ms at 16,384); N = 2 up to 16,384; N = 5 up to
-// 6,144; N = 8 except near 6,144.
-bool nbody8_auto(int NB, int64_t batch) {
+// IRK_OPT_MAPPING auto for the N-body ensembles, from tools/nb_map_ab.py (1,000
+// steps at batches 2,048 / 6,144 / 16,384 / 65,536, all three mappings;
+// profiles/r2/nb_map_ab_r2.json): stage per lane with DMMA contractions
+// (ens_nbody8m) for N = 3..6 at every batch and N = 2 up to 32,768 (config 3:
+// 30.6 vs 39.1 ms shared-memory stage per lane, 46.0 ms body per lane); N = 7, 8
+// keep the round-1 choice (ens_nbody8m's tiles do not fit unpadded in registers
+// and shared memory there: slower): stage per lane for N = 7, and for N = 8
+// except near 6,144; body per lane for N = 2 beyond 32,768.
+int nbody_auto_mapping(int NB, int64_t batch) {
     switch (NB) {
-    case 2: return batch <= 32768;
-    case 5: return batch <= 8192;
-    case 8: return batch <= 4096 || batch >= 12288;
-    default: return true;
+    case 2: return batch <= 32768 ? IRK_MAP_G8M : IRK_MAP_G1;
+    case 7: return IRK_MAP_G8;
+    case 8: return (batch <= 4096 || batch >= 12288) ? IRK_MAP_G8 : IRK_MAP_G1;
+    default: return IRK_MAP_G8M;
     }
 }
 
@@ -743,23 +747,28 @@ int launch_nbody_t(irk_ctx *c, double *y, double t0, char *ws, double *energy, i
     const int64_t blocks = (c->batch + GPW * WPB - 1) / (GPW * WPB);
     // stage-per-lane (ensemble_nbody8.cuh) when asked or where auto measured it faster; the
     // chunked schedule (IRK_OPT_SCHEDULE = 1) keeps body-per-lane
-    const bool stage_per_lane =
-        c->mapping == IRK_MAP_G8 || (c->mapping == IRK_MAP_AUTO && c->schedule != 1 && nbody8_auto(NB, c->batch));
-    const bool dmma = c->mapping == IRK_MAP_G8M;
+    const int autom = (c->mapping == IRK_MAP_AUTO && c->schedule != 1) ? nbody_auto_mapping(NB, c->batch) : 0;
+    const bool stage_per_lane = c->mapping == IRK_MAP_G8 || autom == IRK_MAP_G8;
+    const bool dmma = c->mapping == IRK_MAP_G8M || autom == IRK_MAP_G8M;
     c->mapping_used = dmma ? IRK_MAP_G8M : stage_per_lane ? IRK_MAP_G8 : IRK_MAP_G1;
     if (dmma) {
+        // units of 50 steps at every batch: a slot's 4 trajectories restart in step at
+        // each unit (they share the contraction's coefficient fragment; drifted apart,
+        // the velocity contraction runs twice): config 3 1.70 s with 32 units per
+        // trajectory (1,563 steps), 1.58 / 1.53 / 1.52 / 1.53 s at 250 / 100 / 50 / 25
+        constexpr int64_t kUnitSteps = 50;
         constexpr int SPB = irk::N8M_THREADS / 32 * 4;  // trajectories per block
         return (IRK_UNIT_G && P.G == 1.0)
                    ? launch_queue(c, irk::ens_nbody8m_kernel<NB, true>, irk::N8M_THREADS, SPB,
                                   &c->nbody8m_blocks_per_sm[NB], a, ws, st,
                                   [&](const EnsArgs &aa, const irk::QueueArgs &qa, unsigned nb) {
                                       irk::ens_nbody8m_kernel<NB, true><<<nb, irk::N8M_THREADS, 0, st>>>(aa, qa, P);
-                                  })
+                                  }, 32, 0, kUnitSteps)
                    : launch_queue(c, irk::ens_nbody8m_kernel<NB, false>, irk::N8M_THREADS, SPB,
                                   &c->nbody8m_blocks_per_sm[NB], a, ws, st,
                                   [&](const EnsArgs &aa, const irk::QueueArgs &qa, unsigned nb) {
                                       irk::ens_nbody8m_kernel<NB, false><<<nb, irk::N8M_THREADS, 0, st>>>(aa, qa, P);
-                                  });
+                                  }, 32, 0, kUnitSteps);
     }
     if (stage_per_lane)
         return (IRK_UNIT_G && P.G == 1.0)

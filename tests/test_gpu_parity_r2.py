@@ -87,13 +87,15 @@ def test_config5_n1024_full_1000_steps(irk, orc):
 # ------------------------------------------------------ resolved mapping
 @pytest.mark.parametrize("problem,batch,expect", [
     ("kepler", 1, 8), ("kepler", 4096, 8), ("kepler", 8192, 4), ("kepler", 65536, 1),
-    ("fpu", 64, 0), ("plummer", 1, 0)])
+    ("fpu", 64, 0), ("plummer", 1, 0), ("sixbody", 16384, 9), ("sixbody", 1, 9)])
 def test_mapping_used_info(irk, problem, batch, expect):
     """IRK_INFO_MAPPING_USED reports what IRK_OPT_MAPPING auto resolved to."""
     if problem == "kepler":
         w = wl.kepler_ensemble(batch=batch, nsteps=3)
     elif problem == "fpu":
         w = wl.fpu_ensemble(batch=batch, nsteps=3)
+    elif problem == "sixbody":
+        w = wl.six_body_ensemble(batch=batch, nsteps=3)
     else:
         w = wl.plummer(N=1024, nsteps=1)
     with irk.Integrator(w.problem, w.dim, w.h, w.nsteps, w.batch, w.params) as ig:
