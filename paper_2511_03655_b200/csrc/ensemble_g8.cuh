@@ -59,11 +59,11 @@ __global__ void __maxnreg__(G8_MAXREG) ens_gs_kernel(const __grid_constant__ Ens
     // (Kept in registers they were rematerialised from the constant bank with
     // lane-divergent addresses: serialised LDC, ncu mio_throttle.)
     __shared__ double sW[72 + 64], sHB[8], sC[8];
-#if G8_SMEM
     // per-group all-gather tile [stage][component], groups padded into different banks
-    __shared__ __align__(16) double sG[GPB][8 * d + 2];
+    // (G8_SMEM = 0: shuffles instead, one stage per lane only)
+    constexpr bool SMEM = G8_SMEM || G != 8;
+    __shared__ __align__(16) double sG[GPB][SMEM ? 8 * d + 2 : 2];
     const int gib = threadIdx.x / G;
-#endif
     for (int e = threadIdx.x; e < 64; e += blockDim.x) {
         sW[(e & 7) * 8 + (e >> 3)] = (&c_mu[0][0])[e];       // mu~[i][j] at [j][i]
         sW[72 + (e & 7) * 8 + (e >> 3)] = (&c_nu[0][0])[e];
@@ -136,36 +136,27 @@ __global__ void __maxnreg__(G8_MAXREG) ens_gs_kernel(const __grid_constant__ Ens
         double sLq[d], Qs[SPL][d];  // S(Lq) is formed on the fly (the gathered Lq die here)
         int64_t delta[d];
         bool stop = (k >= 2);
-#if G8_SMEM
-#pragma unroll
-        for (int t = 0; t < SPL; ++t)
-#pragma unroll
-            for (int l = 0; l < d; ++l) sG[gib][(st0 + t) * d + l] = dmul(sHB[st0 + t], Vs[t][l]);
-        __syncwarp();
-#else
-        static_assert(G == 8, "the shuffle all-gather is written for one stage per lane");
         double lq[d];
+        if constexpr (SMEM) {
 #pragma unroll
-        for (int l = 0; l < d; ++l) lq[l] = dmul(sHB[s], Vs[0][l]);
-#endif
+            for (int t = 0; t < SPL; ++t)
+#pragma unroll
+                for (int l = 0; l < d; ++l) sG[gib][(st0 + t) * d + l] = dmul(sHB[st0 + t], Vs[t][l]);
+            __syncwarp();
+        } else {
+#pragma unroll
+            for (int l = 0; l < d; ++l) lq[l] = dmul(sHB[s], Vs[0][l]);
+        }
 #pragma unroll
         for (int l = 0; l < d; ++l) {
-#if G8_SMEM
-            double g = sG[gib][l];
-#else
-            double g = __shfl_sync(FULL, lq[l], base);
-#endif
+            double g = SMEM ? sG[gib][l] : __shfl_sync(FULL, lq[l], base);
             double acc[SPL];
 #pragma unroll
             for (int t = 0; t < SPL; ++t) acc[t] = dmul(Mu[t], g);
             sLq[l] = g;
 #pragma unroll
             for (int j = 1; j < 8; ++j) {
-#if G8_SMEM
-                g = sG[gib][j * d + l];
-#else
-                g = __shfl_sync(FULL, lq[l], base + j);
-#endif
+                g = SMEM ? sG[gib][j * d + l] : __shfl_sync(FULL, lq[l], base + j);
 #pragma unroll
                 for (int t = 0; t < SPL; ++t) acc[t] = dfma(Mu[8 * j + t], g, acc[t]);
                 sLq[l] = dadd(sLq[l], g);
@@ -201,26 +192,26 @@ __global__ void __maxnreg__(G8_MAXREG) ens_gs_kernel(const __grid_constant__ Ens
         }
         // ---- a4 (first half): Lv, all-gather ----
         double Lvg[8][d], Lvs[SPL][d];
-#if G8_SMEM
-        __syncwarp();  // the Lq reads of this sweep are done
+        if constexpr (SMEM) {
+            __syncwarp();  // the Lq reads of this sweep are done
 #pragma unroll
-        for (int t = 0; t < SPL; ++t)
+            for (int t = 0; t < SPL; ++t)
 #pragma unroll
-            for (int l = 0; l < d; ++l) sG[gib][(st0 + t) * d + l] = Lvs[t][l] = dmul(sHB[st0 + t], Fs[t][l]);
-        __syncwarp();
+                for (int l = 0; l < d; ++l) sG[gib][(st0 + t) * d + l] = Lvs[t][l] = dmul(sHB[st0 + t], Fs[t][l]);
+            __syncwarp();
 #pragma unroll
-        for (int j = 0; j < 8; ++j)
+            for (int j = 0; j < 8; ++j)
 #pragma unroll
-            for (int l = 0; l < d; ++l) Lvg[j][l] = sG[gib][j * d + l];
-        __syncwarp();  // before the next sweep's writes
-#else
+                for (int l = 0; l < d; ++l) Lvg[j][l] = sG[gib][j * d + l];
+            __syncwarp();  // before the next sweep's writes
+        } else {
 #pragma unroll
-        for (int l = 0; l < d; ++l) {
-            Lvs[0][l] = dmul(sHB[s], Fs[0][l]);
+            for (int l = 0; l < d; ++l) {
+                Lvs[0][l] = dmul(sHB[s], Fs[0][l]);
 #pragma unroll
-            for (int j = 0; j < 8; ++j) Lvg[j][l] = __shfl_sync(FULL, Lvs[0][l], base + j);
+                for (int j = 0; j < 8; ++j) Lvg[j][l] = __shfl_sync(FULL, Lvs[0][l], base + j);
+            }
         }
-#endif
         // the stop test after the right-hand sides: the RHS does not need it, so the
         // Delta shuffles and the RHS chains share one basic block and overlap
         {   // reading R2, on the bit patterns as in ens_g1q; branch-free so
