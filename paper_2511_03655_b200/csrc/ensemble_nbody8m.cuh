@@ -54,7 +54,10 @@
 
 namespace irk {
 
-constexpr int N8M_THREADS = 64;  // 2 warps = 2 slots = 8 trajectories per block
+#ifndef N8M_WARPS
+#define N8M_WARPS 2
+#endif
+constexpr int N8M_THREADS = 32 * N8M_WARPS;  // one slot of 4 trajectories per warp
 #ifndef N8M_MAXREG
 #define N8M_MAXREG 168
 #endif
