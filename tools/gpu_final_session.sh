@@ -1,4 +1,5 @@
 # final measurement session: GPU tests, bench line, launch list, ncu --set full of the bench kernel
+# and of the config-3 kernel, strong-scaling projection (profiles/r2)
 set -x
 mkdir -p gpurun_out
 timeout 1500 python -m pytest tests -m gpu -q > gpurun_out/pytest_final.log 2>&1; echo pytest rc=$?
@@ -9,6 +10,6 @@ timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --c
 python tools/run_once.py --config 2 > gpurun_out/plain_final.log 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:ens_g1q -c 1 -o gpurun_out/g1q_final python tools/run_once.py --config 2 > gpurun_out/ncu_full.log 2>&1; echo ncu2 rc=$?
 ncu -i gpurun_out/g1q_final.ncu-rep --page raw --csv > gpurun_out/g1q_final_raw.csv 2>/dev/null
-ncu -i gpurun_out/g1q_final.ncu-rep --page source --csv --print-source cuda,sass > gpurun_out/g1q_final_src.csv 2>/dev/null
 rm -f gpurun_out/g1q_final.ncu-rep
+timeout 600 bash tools/ncu_src.sh 3 2000 ens_nbody8m nb8m_final; echo ncu3 rc=$?
 timeout 1200 python tools/strong_scaling.py gpurun_out/strong_scaling_final.json > gpurun_out/strong_scaling_final.log 2>&1; echo ss rc=$?
