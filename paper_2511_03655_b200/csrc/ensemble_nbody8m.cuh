@@ -67,6 +67,9 @@ constexpr int N8M_THREADS = 32 * N8M_WARPS;  // one slot of 4 trajectories per w
 #ifndef N8M_A2SYNC
 #define N8M_A2SYNC 0
 #endif
+#ifndef N8M_QKEEP
+#define N8M_QKEEP 1  // Q_s of this sweep kept in registers from a2 to the RHS (-1.3 %)
+#endif
 #ifndef N8M_QSMEM
 #define N8M_QSMEM 1  // stage positions Q between sweeps in shared memory ([component][lane]), not registers
 #endif
@@ -302,6 +305,9 @@ __global__ void __maxnreg__(N8M_MAXREG) ens_nbody8m_kernel(const __grid_constant
         const bool anyk2 = __any_sync(FULL, k2);
         __syncwarp();  // Lq rows written
         // ---- a2: Q_s = q + D(mu_s., Lq) ; |Q_s - Q_s^old| -> own row of E ----
+#if N8M_QKEEP
+        double Qk[d2];  // this sweep's Q_s, kept for the RHS (the shared copy is next sweep's Q^old)
+#endif
         {
             double b0[T], b1[T], Dq[d2];
             n8m_frags<T>(X, fb0, fb1, b0, b1);
@@ -320,6 +326,10 @@ __global__ void __maxnreg__(N8M_MAXREG) ens_nbody8m_kernel(const __grid_constant
                 if (anyk2) *reinterpret_cast<longlong2 *>(&E[myrow + 2 * t]) = e;
                 N8M_Q(2 * t) = q0;
                 N8M_Q(2 * t + 1) = q1;
+#if N8M_QKEEP
+                Qk[2 * t] = q0;
+                Qk[2 * t + 1] = q1;
+#endif
             }
         }
         __syncwarp();  // E rows written
@@ -351,7 +361,13 @@ __global__ void __maxnreg__(N8M_MAXREG) ens_nbody8m_kernel(const __grid_constant
         {
             double F[d], Qs[d];
 #pragma unroll
-            for (int l = 0; l < d; ++l) Qs[l] = N8M_Q(l);
+            for (int l = 0; l < d; ++l) {
+#if N8M_QKEEP
+                Qs[l] = Qk[l];
+#else
+                Qs[l] = N8M_Q(l);
+#endif
+            }
             bool ok = true;
 #if N8M_DREUSE
             n8m_accel<NB, G1>(Qs, F, P, sm, ok);

@@ -108,3 +108,40 @@ def test_dmma_config3_full_batch_vs_g8(irk):
     g9 = run_gpu(irk, w, mapping=irk.MAP_G8M)
     g8 = run_gpu(irk, w, mapping=irk.MAP_G8)
     assert np.array_equal(g9["y"], g8["y"]) and np.array_equal(g9["iters"], g8["iters"])
+
+
+def test_dmma_max_iters_cap_mixed_slots(irk, orc):
+    """max_iters = 3 on heterogeneous systems: trajectories of a slot hit the cap or
+    converge at different sweeps (the mixed mu~ / nu~ velocity pass), flagged and
+    bitwise like the oracle."""
+    rng = np.random.default_rng(11)
+    N, B = 6, 45
+    q = rng.standard_normal((3 * N, B)) * rng.uniform(0.3, 3.0, B)
+    v = 0.4 * rng.standard_normal((3 * N, B))
+    params = np.concatenate([[1.0, 0.02], rng.uniform(0.2, 1.0, N)])
+    w = wl.Workload("nb6_hetero", wl.NBODY, 6 * N, np.concatenate([q, v]), params, 0.02, 120)
+    g = run_gpu(irk, w, max_iters=3, mapping=irk.MAP_G8M)
+    o = orc.integrate(w.problem, w.y, w.params, w.h, w.nsteps, max_iters=3)
+    assert_parity(g, o)
+    assert g["stats"]["maxiter_traj"] == int((o["status"][:, 0] > 0).sum()) > 0
+
+
+def test_dmma_divergence_flag_and_freeze(irk, orc):
+    """Two bodies at the same position and velocity with eps = 0 in one trajectory of a slot:
+    the weight is infinite, the step non-finite; the trajectory is flagged at the
+    oracle's step and frozen, its slot partners are unaffected (bitwise)."""
+    w = wl.six_body_ensemble(batch=7, nsteps=40)
+    w.params = np.asarray(w.params, dtype=np.float64).copy()
+    w.params[1] = 0.0
+    y = np.asarray(w.y, dtype=np.float64).copy()
+    y[3:6, 2] = y[0:3, 2]      # body 1 on body 0 in trajectory 2,
+    y[21:24, 2] = y[18:21, 2]  # with the same velocity: they coincide at every stage
+    w.y = y
+    g = run_gpu(irk, w, mapping=irk.MAP_G8M)
+    o = orc.integrate(w.problem, y, w.params, w.h, w.nsteps)
+    assert g["rc"] == irk.E_DIVERGED
+    assert g["stats"]["diverged_traj"] == 1
+    assert g["stats"]["first_bad_step"] == o["status"][2, 1]
+    keep = [b for b in range(w.batch) if b != 2]
+    np.testing.assert_array_equal(g["y"][:, keep], o["y"][:, keep])
+    np.testing.assert_array_equal(g["iters"][keep], o["iters"][keep])
