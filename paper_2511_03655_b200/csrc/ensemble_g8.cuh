@@ -75,6 +75,24 @@ __global__ void __maxnreg__(G8_MAXREG) ens_gs_kernel(const __grid_constant__ Ens
     __syncthreads();
     const int st0 = s * SPL;                           // first owned stage
     const double *Mu = sW + st0, *Nu = sW + 72 + st0;  // coefficient (st0 + t, j) at [8 j + t]
+    // g8 keeps its lane's coefficient rows mu~_s., nu~_s. and hb_s in registers (16 + 1
+    // doubles): 18 fewer shared loads per sweep on the single-trajectory critical
+    // path.  The values pass through an empty asm so that the compiler cannot
+    // re-load them from shared memory inside the loop.
+    constexpr bool CREG = (G == 8);
+    double rMu[8], rNu[8], rHB[SPL];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+        rMu[j] = CREG ? Mu[8 * j] : 0.0;
+        rNu[j] = CREG ? Nu[8 * j] : 0.0;
+        asm("" : "+d"(rMu[j]), "+d"(rNu[j]));
+    }
+#pragma unroll
+    for (int t = 0; t < SPL; ++t) {
+        rHB[t] = sHB[st0 + t];
+        asm("" : "+d"(rHB[t]));
+    }
+    auto MU = [&](int j, int t) -> double { return CREG ? rMu[j] : Mu[8 * j + t]; };
 
     double q[d], v[d];
 #pragma unroll
@@ -141,24 +159,24 @@ __global__ void __maxnreg__(G8_MAXREG) ens_gs_kernel(const __grid_constant__ Ens
 #pragma unroll
             for (int t = 0; t < SPL; ++t)
 #pragma unroll
-                for (int l = 0; l < d; ++l) sG[gib][(st0 + t) * d + l] = dmul(sHB[st0 + t], Vs[t][l]);
+                for (int l = 0; l < d; ++l) sG[gib][(st0 + t) * d + l] = dmul(rHB[t], Vs[t][l]);
             __syncwarp();
         } else {
 #pragma unroll
-            for (int l = 0; l < d; ++l) lq[l] = dmul(sHB[s], Vs[0][l]);
+            for (int l = 0; l < d; ++l) lq[l] = dmul(rHB[0], Vs[0][l]);
         }
 #pragma unroll
         for (int l = 0; l < d; ++l) {
             double g = SMEM ? sG[gib][l] : __shfl_sync(FULL, lq[l], base);
             double acc[SPL];
 #pragma unroll
-            for (int t = 0; t < SPL; ++t) acc[t] = dmul(Mu[t], g);
+            for (int t = 0; t < SPL; ++t) acc[t] = dmul(MU(0, t), g);
             sLq[l] = g;
 #pragma unroll
             for (int j = 1; j < 8; ++j) {
                 g = SMEM ? sG[gib][j * d + l] : __shfl_sync(FULL, lq[l], base + j);
 #pragma unroll
-                for (int t = 0; t < SPL; ++t) acc[t] = dfma(Mu[8 * j + t], g, acc[t]);
+                for (int t = 0; t < SPL; ++t) acc[t] = dfma(MU(j, t), g, acc[t]);
                 sLq[l] = dadd(sLq[l], g);
             }
             int64_t e = 0;
@@ -197,7 +215,7 @@ __global__ void __maxnreg__(G8_MAXREG) ens_gs_kernel(const __grid_constant__ Ens
 #pragma unroll
             for (int t = 0; t < SPL; ++t)
 #pragma unroll
-                for (int l = 0; l < d; ++l) sG[gib][(st0 + t) * d + l] = Lvs[t][l] = dmul(sHB[st0 + t], Fs[t][l]);
+                for (int l = 0; l < d; ++l) sG[gib][(st0 + t) * d + l] = Lvs[t][l] = dmul(rHB[t], Fs[t][l]);
             __syncwarp();
 #pragma unroll
             for (int j = 0; j < 8; ++j)
@@ -207,7 +225,7 @@ __global__ void __maxnreg__(G8_MAXREG) ens_gs_kernel(const __grid_constant__ Ens
         } else {
 #pragma unroll
             for (int l = 0; l < d; ++l) {
-                Lvs[0][l] = dmul(sHB[s], Fs[0][l]);
+                Lvs[0][l] = dmul(rHB[0], Fs[0][l]);
 #pragma unroll
                 for (int j = 0; j < 8; ++j) Lvg[j][l] = __shfl_sync(FULL, Lvs[0][l], base + j);
             }
@@ -228,15 +246,39 @@ __global__ void __maxnreg__(G8_MAXREG) ens_gs_kernel(const __grid_constant__ Ens
             }
         }
         const bool fin = live && (stop || k >= a.max_iters);
+        // ---- a4 (second half) / next step's a1, contraction part: D(W_i., Lv), W = nu
+        // when the step finishes.  Formed before the update so that its chain runs
+        // beside the S(Lv) chain of a6 (only the final v + D depends on the update).
+        double accV[SPL][d];
+        {
+            const double *W = fin ? Nu : Mu;
+            double rW[8];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) rW[j] = fin ? rNu[j] : rMu[j];
+#pragma unroll
+            for (int l = 0; l < d; ++l)
+#pragma unroll
+                for (int t = 0; t < SPL; ++t) {
+                    double acc = dmul(CREG ? rW[0] : W[t], Lvg[0][l]);
+#pragma unroll
+                    for (int j = 1; j < 8; ++j) acc = dfma(CREG ? rW[j] : W[8 * j + t], Lvg[j][l], acc);
+                    accV[t][l] = acc;
+                }
+        }
+        // S(Lv) of a6, formed every sweep beside the chain above (off the update's path)
+        double sv[d];
+#pragma unroll
+        for (int l = 0; l < d; ++l) {
+            sv[l] = Lvg[0][l];
+#pragma unroll
+            for (int j = 1; j < 8; ++j) sv[l] = dadd(sv[l], Lvg[j][l]);
+        }
         if (fin) {  // ---- a6: update (replicated in the group), history, samples ----
             bool finite = true;
 #pragma unroll
             for (int l = 0; l < d; ++l) {
-                double sv = Lvg[0][l];
-#pragma unroll
-                for (int j = 1; j < 8; ++j) sv = dadd(sv, Lvg[j][l]);
                 q[l] = dadd(q[l], sLq[l]);
-                v[l] = dadd(v[l], sv);
+                v[l] = dadd(v[l], sv[l]);
                 finite = finite && isfinite(q[l]) && isfinite(v[l]);
             }
             ++n;
@@ -263,18 +305,10 @@ __global__ void __maxnreg__(G8_MAXREG) ens_gs_kernel(const __grid_constant__ Ens
             }
         }
         // ---- a4 (second half) / next step's a1: V_i = v + D(W_i., Lv) ----
-        {
-            const double *W = fin ? Nu : Mu;
 #pragma unroll
-            for (int l = 0; l < d; ++l)
+        for (int l = 0; l < d; ++l)
 #pragma unroll
-                for (int t = 0; t < SPL; ++t) {
-                    double acc = dmul(W[t], Lvg[0][l]);
-#pragma unroll
-                    for (int j = 1; j < 8; ++j) acc = dfma(W[8 * j + t], Lvg[j][l], acc);
-                    Vs[t][l] = dadd(v[l], acc);
-                }
-        }
+            for (int t = 0; t < SPL; ++t) Vs[t][l] = dadd(v[l], accV[t][l]);
     }
     if (valid && s == 0) {
 #pragma unroll
