@@ -48,7 +48,8 @@ UNIT = "traj-steps/s"
 SM_COUNT = 148
 FP64_FMA_PER_CLK_PER_SM = 64  # B200 (sm_100a) non-tensor FP64 rate
 MAP_NAMES = {0: "single mapping", 1: "g1 (1 trajectory per thread / body per lane)", 2: "g2 (4 stages per lane)",
-             4: "g4 (2 stages per lane)", 8: "g8 (1 stage per lane)"}
+             4: "g4 (2 stages per lane)", 8: "g8 (1 stage per lane)",
+             9: "g8m (1 stage per lane, DMMA stage contractions)"}
 
 
 # --------------------------------------------------------------- flop model

@@ -20,7 +20,7 @@ LIB = os.path.join(OUT, "libirk.so")
 
 CU_SOURCES = ["irk_api.cu", "probe.cu"]
 CPP_SOURCES = ["tableau.cpp"]
-HEADERS = ["fp64.cuh", "problems.cuh", "ens_common.cuh", "ensemble_g1.cuh", "ensemble_g8.cuh", "ensemble_fo.cuh", "ensemble_nbody.cuh", "ensemble_nbody8.cuh", "ensemble_chain.cuh", "nbody_direct.cuh",
+HEADERS = ["fp64.cuh", "problems.cuh", "ens_common.cuh", "ensemble_g1.cuh", "ensemble_g8.cuh", "ensemble_fo.cuh", "ensemble_nbody.cuh", "ensemble_nbody8.cuh", "ensemble_nbody8m.cuh", "ensemble_g8m.cuh", "ensemble_chain.cuh", "nbody_direct.cuh",
            "balance.cuh",
            "tableau.h"]
 

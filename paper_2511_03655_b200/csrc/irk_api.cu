@@ -24,6 +24,7 @@
 #endif
 #include "ensemble_g1.cuh"
 #include "ensemble_g8.cuh"
+#include "ensemble_g8m.cuh"
 #include "ensemble_fo.cuh"
 #include "ensemble_nbody.cuh"
 #include "ensemble_nbody8.cuh"
@@ -98,7 +99,9 @@ constexpr size_t kHeader = 64;
 #ifndef IRK_G2_AUTO_MAX
 #define IRK_G2_AUTO_MAX 0  // g2 is not chosen by auto any more (g1 on 2 blocks per SM beats it)
 #endif
-// IRK_OPT_MAPPING auto (Kepler, HH): g8 up to kG8AutoMaxBatch, g4 up to kG4AutoMaxBatch, then g1
+// IRK_OPT_MAPPING auto (Kepler, HH): g8m (stage per lane, DMMA contractions; faster than
+// g8 at every batch up to 8,192: config 1 13.8 -> 13.1 ms, 6,144: 22.2 -> 20.9 ms) up to
+// kG8AutoMaxBatch, g4 up to kG4AutoMaxBatch, then g1
 // (ens_g1q, launch geometry in launch_g1q).  Measured with tools/ab.py, config-2 generator,
 // 10,000 steps (profiles/r2/ab_mapping_crossover.json), g1 / g2 / g4 / g8 ms:
 // 4,096: 38.9/31.2/22.2/19.3; 6,144: 38.9/31.6/26.8/23.9; 8,192: 38.7/31.5/27.0/29.6;
@@ -657,6 +660,26 @@ int launch_gs(irk_ctx *c, const P &prob, EnsArgs &a, char *ws, cudaStream_t st) 
     return cuda_check(c, cudaGetLastError(), "advance_n launch");
 }
 
+// Stage per lane with DMMA contractions (ensemble_g8m.cuh): one launch, one slot of
+// 4 trajectories per warp.
+template <class P>
+int launch_gsm(irk_ctx *c, const P &prob, EnsArgs &a, char *ws, cudaStream_t st) {
+    a.nsteps = c->nsteps;
+    a.c0 = 0;
+    a.csweeps = nullptr;
+    a.perm = nullptr;
+    a.nslots = c->batch;
+    const int64_t blocks = (c->batch * 8 + irk::G8M_THREADS - 1) / irk::G8M_THREADS;
+    if (c->batch <= 4)  // one slot: the latency-bound single-trajectory case (config 1)
+        irk::ens_gsm_kernel<P, true, false><<<(unsigned)blocks, irk::G8M_THREADS, 0, st>>>(a, prob);
+    else
+        irk::ens_gsm_kernel<P, false, true><<<(unsigned)blocks, irk::G8M_THREADS, 0, st>>>(a, prob);
+    int rc = cuda_check(c, cudaGetLastError(), "ens_gsm launch");
+    if (rc) return rc;
+    advance_n_kernel<<<1, 1, 0, st>>>(reinterpret_cast<int64_t *>(ws), c->nsteps);
+    return cuda_check(c, cudaGetLastError(), "advance_n launch");
+}
+
 // IRK_OPT_MAPPING auto for the N-body ensembles, from tools/nb_map_ab.py (1,000
 // steps at batches 2,048 / 6,144 / 16,384 / 65,536, all three mappings;
 // profiles/r2/nb_map_ab_r2.json): stage per lane with DMMA contractions
@@ -678,11 +701,12 @@ int nbody_auto_mapping(int NB, int64_t batch) {
 // trajectory G = 8 while the batch leaves most g1 lanes of the GPU empty, then
 // G = 4, then one trajectory per lane ("ens_gs": measured crossovers).
 int lanes_per_trajectory(const irk_ctx *c) {
+    if (c->mapping == IRK_MAP_G8M) return IRK_MAP_G8M;
     if (c->mapping == IRK_MAP_G8) return 8;
     if (c->mapping == IRK_MAP_G4) return 4;
     if (c->mapping == IRK_MAP_G2) return 2;
     if (c->mapping == IRK_MAP_G1) return 1;
-    if (c->batch <= kG8AutoMaxBatch) return 8;
+    if (c->batch <= kG8AutoMaxBatch) return IRK_MAP_G8M;
     if (c->batch <= kG4AutoMaxBatch) return 4;
     if (c->batch > kG4AutoMaxBatch * 5 / 4 && c->batch <= kG2AutoMaxBatch) return 2;  // g1 ~ g4 in between
     return 1;
@@ -726,6 +750,7 @@ int launch_g1(irk_ctx *c, const P &prob, double *y, double t0, char *ws, double 
     EnsArgs a = ens_args(c, y, t0, ws, energy, iters);
     const int64_t blocks = (c->batch + irk::G1_THREADS - 1) / irk::G1_THREADS;
     c->mapping_used = c->mode == 0 ? lanes_per_trajectory(c) : IRK_MAP_G1;  // (first-order: set below)
+    if (c->mode == 0 && lanes_per_trajectory(c) == IRK_MAP_G8M) return launch_gsm(c, prob, a, ws, st);
     if (c->mode == 0 && lanes_per_trajectory(c) == 8) return launch_gs<P, 8>(c, prob, a, ws, st);
     if (c->mode == 0 && lanes_per_trajectory(c) == 4) return launch_gs<P, 4>(c, prob, a, ws, st);
     if (c->mode == 0 && lanes_per_trajectory(c) == 2) return launch_gs<P, 2>(c, prob, a, ws, st);
@@ -1134,8 +1159,8 @@ int irk_set_option(irk_ctx *c, int key, int64_t val) {
             val != IRK_MAP_G8M)
             return fail(c, IRK_E_ARG,
                         "irk_set_option: MAPPING must be 0 (auto), 1 (g1), 2 (g2), 4 (g4), 8 (g8) or 9 (g8m)");
-        if (val == IRK_MAP_G8M && c->problem != IRK_NBODY)
-            return fail(c, IRK_E_ARG, "irk_set_option: the g8m mapping is built for the N-body ensembles");
+        if (val == IRK_MAP_G8M && c->problem != IRK_NBODY && c->problem != IRK_KEPLER && c->problem != IRK_HENON_HEILES)
+            return fail(c, IRK_E_ARG, "irk_set_option: the g8m mapping is built for Kepler, Henon-Heiles, N-body");
         if ((val == IRK_MAP_G4 || val == IRK_MAP_G2) && c->problem != IRK_KEPLER && c->problem != IRK_HENON_HEILES)
             return fail(c, IRK_E_ARG, "irk_set_option: the g2 / g4 mappings are built for Kepler and Henon-Heiles");
         if (val == IRK_MAP_G8 && c->problem != IRK_KEPLER && c->problem != IRK_HENON_HEILES && c->problem != IRK_NBODY &&

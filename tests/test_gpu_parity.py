@@ -311,11 +311,12 @@ def test_work_queue_chain_bitwise(irk, orc):
     assert np.array_equal(outs[1][2][idx], orr["iters"]) and np.array_equal(outs[1][4][idx], orr["dhloc"])
 
 
-@pytest.mark.parametrize("G", [8, 4, 2])
+@pytest.mark.parametrize("G", [8, 4, 2, 9])
 @pytest.mark.parametrize("which", ["kepler", "hh"])
 def test_g8_stage_per_lane_mapping(irk, orc, which, G):
     """IRK_OPT_MAPPING = 8 / 4 / 2 (G lanes per trajectory, 8/G stages per lane,
-    shared-memory all-gather, xor-shuffle Delta reduction): bitwise equal to the
+    shared-memory all-gather, xor-shuffle Delta reduction) and 9 (g8m: stage per
+    lane, DMMA contractions): bitwise equal to the
     oracle and to g1 -- states, sweeps, energy samples, Delta H^loc, a diverging
     trajectory, and two chained calls."""
     if which == "kepler":

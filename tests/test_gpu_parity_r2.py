@@ -33,7 +33,7 @@ def _with_params(w, params):
 
 
 # ------------------------------------------------------ G != 1 instantiations
-@pytest.mark.parametrize("mapping", [1, 2, 4, 8])
+@pytest.mark.parametrize("mapping", [1, 2, 4, 8, 9])
 def test_kepler_gm_not_one_every_mapping(irk, orc, mapping):
     """Kepler with GM = 1.3 runs KeplerT<false> (the full correctly rounded
     division w = GM / r^3, Eq. of the Kepler functor in CANON.md) in every
@@ -86,7 +86,7 @@ def test_config5_n1024_full_1000_steps(irk, orc):
 
 # ------------------------------------------------------ resolved mapping
 @pytest.mark.parametrize("problem,batch,expect", [
-    ("kepler", 1, 8), ("kepler", 4096, 8), ("kepler", 8192, 4), ("kepler", 65536, 1),
+    ("kepler", 1, 9), ("kepler", 4096, 9), ("kepler", 8192, 4), ("kepler", 65536, 1),
     ("fpu", 64, 0), ("plummer", 1, 0), ("sixbody", 16384, 9), ("sixbody", 1, 9)])
 def test_mapping_used_info(irk, problem, batch, expect):
     """IRK_INFO_MAPPING_USED reports what IRK_OPT_MAPPING auto resolved to."""
