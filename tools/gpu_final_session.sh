@@ -12,4 +12,5 @@ timeout 900 ncu --set full --clock-control none --import-source on -k regex:ens_
 ncu -i gpurun_out/g1q_final.ncu-rep --page raw --csv > gpurun_out/g1q_final_raw.csv 2>/dev/null
 rm -f gpurun_out/g1q_final.ncu-rep
 timeout 600 bash tools/ncu_src.sh 3 2000 ens_nbody8m nb8m_final; echo ncu3 rc=$?
+timeout 600 bash tools/ncu_src.sh 1 0 ens_gsm c1_g8m_final; echo ncu4 rc=$?
 timeout 1200 python tools/strong_scaling.py gpurun_out/strong_scaling_final.json > gpurun_out/strong_scaling_final.log 2>&1; echo ss rc=$?
