@@ -376,13 +376,13 @@ int launch_direct(irk_ctx *c, double *y, double t0, char *ws, double *energy, in
             if (r) return r;
         }
         for (int t = 0; t < nlocal; ++t)
-            irk::nbd_energy_terms_kernel<<<(unsigned)((nloc + 127) / 128), 128, 0, st>>>(
+            irk::nbd_energy_terms_kernel<<<(unsigned)((nloc + irk::NBD_EROW_ROWS - 1) / irk::NBD_EROW_ROWS), irk::NBD_EROW_THREADS, 0, st>>>(
                 Qall, A[t].yv, c->d_mass, N, A[t].b0, nloc, A[t].G, A[t].eps2, terms + 2 * A[t].b0);
         if (nccl) {
             int r = nccl_allgather_inplace(c, terms, (size_t)(2 * nloc), st);
             if (r) return r;
         }
-        irk::nbd_energy_sum_kernel<<<1, 1, 0, st>>>(terms, P, nloc, energy + idx);
+        irk::nbd_energy_sum_kernel<<<1, irk::NBD_ESUM_THREADS, 0, st>>>(terms, P, nloc, energy + idx);
         return cuda_check(c, cudaGetLastError(), "energy sample");
     };
     if (E > 0 && energy && (rc = sample(0))) return rc;
@@ -1339,10 +1339,10 @@ int irk_energy(irk_ctx *c, const double *y, double *H, void *stream) {
             return rc;
         if (c->nccl_comm && (rc = nccl_allgather_inplace(c, Qall, (size_t)(3 * nloc), st))) return rc;
         const double *v = y + (c->nccl_comm ? 3 * nloc : 3 * N);
-        irk::nbd_energy_terms_kernel<<<(unsigned)((nloc + 127) / 128), 128, 0, st>>>(
+        irk::nbd_energy_terms_kernel<<<(unsigned)((nloc + irk::NBD_EROW_ROWS - 1) / irk::NBD_EROW_ROWS), irk::NBD_EROW_THREADS, 0, st>>>(
             Qall, v, c->d_mass, N, b0, nloc, c->params[0], c->params[1] * c->params[1], terms + 2 * b0);
         if (c->nccl_comm && (rc = nccl_allgather_inplace(c, terms, (size_t)(2 * nloc), st))) return rc;
-        irk::nbd_energy_sum_kernel<<<1, 1, 0, st>>>(terms, P, nloc, H);
+        irk::nbd_energy_sum_kernel<<<1, irk::NBD_ESUM_THREADS, 0, st>>>(terms, P, nloc, H);
         break;
     }
     case IRK_FPU_BETA: {

@@ -534,33 +534,80 @@ __global__ void nbd_xfinal_kernel(const __grid_constant__ NbdArgs a, int64_t *n_
 // ---- energy (canonical: kinetic terms, then row sums over j > i, Neumaier) ----
 // Qall: all N positions (3N, gathered); each shard writes its kinetic terms and
 // row sums into its slot [kin(nloc) | row(nloc)] of `terms` ([P][2*nloc]); the
-// total is added by one thread over all kinetic terms, then all rows, in order.
-__global__ void nbd_energy_terms_kernel(const double *Qall, const double *vloc, const double *mass, int64_t N,
-                                        int64_t b0, int64_t nloc, double G, double eps2, double *slot) {
-    const int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (r >= nloc) return;
-    const int64_t i = b0 + r;
-    const double *q = Qall, *v = vloc + 3 * r;
-    const double k = dfma(v[2], v[2], dfma(v[1], v[1], dmul(v[0], v[0])));
-    slot[r] = dmul(dmul(0.5, mass[i]), k);
-    Neumaier row;
-    for (int64_t j = i + 1; j < N; ++j) {
-        const double dx = dsub(q[3 * j], q[3 * i]);
-        const double dy = dsub(q[3 * j + 1], q[3 * i + 1]);
-        const double dz = dsub(q[3 * j + 2], q[3 * i + 2]);
-        const double r2 = dfma(dz, dz, dfma(dy, dy, dfma(dx, dx, eps2)));
-        row.add(-ddiv(dmul(G, dmul(mass[i], mass[j])), dsqrt(r2)));
+// total is added by one thread over all kinetic terms, then all rows, in order
+// (one compensated sum in the oracle's order: sequential by definition).
+// Row r of the shard (body i = b0 + r) is the in-order Neumaier sum over j > i of
+// -G m_i m_j / sqrt(r_ij^2 + eps^2).  The terms of a row are independent, only
+// their sum is sequential: a block takes 32 rows, its 256 threads evaluate the
+// terms of a 32 x 128 tile (rows x consecutive j) into shared memory, and lane r of
+// warp 0 adds row r's 128 terms in j order -- the same Neumaier sequence, so the
+// same bits as one thread per row, with the divisions and square roots of a tile
+// in flight at once.  Launch ceil(nloc / 32) blocks of NBD_EROW_THREADS threads.
+constexpr int NBD_EROW_THREADS = 256, NBD_EROW_ROWS = 32, NBD_EROW_COLS = 128;
+__global__ void __launch_bounds__(NBD_EROW_THREADS) nbd_energy_terms_kernel(const double *Qall, const double *vloc,
+                                                                            const double *mass, int64_t N, int64_t b0,
+                                                                            int64_t nloc, double G, double eps2,
+                                                                            double *slot) {
+    __shared__ double T[NBD_EROW_ROWS][NBD_EROW_COLS + 1];
+    const double *q = Qall;
+    const int64_t r0 = (int64_t)blockIdx.x * NBD_EROW_ROWS;
+    const int tx = threadIdx.x;
+    if (tx < NBD_EROW_ROWS && r0 + tx < nloc) {  // kinetic terms
+        const int64_t r = r0 + tx;
+        const double *v = vloc + 3 * r;
+        const double k = dfma(v[2], v[2], dfma(v[1], v[1], dmul(v[0], v[0])));
+        slot[r] = dmul(dmul(0.5, mass[b0 + r]), k);
     }
-    slot[nloc + r] = row.result();
+    Neumaier row;  // (lane tx < 32 of warp 0: row r0 + tx)
+    const int64_t ilo = b0 + r0;
+    for (int64_t jc = ilo + 1; jc < N; jc += NBD_EROW_COLS) {
+        for (int e = tx; e < NBD_EROW_ROWS * NBD_EROW_COLS; e += NBD_EROW_THREADS) {
+            const int rr = e / NBD_EROW_COLS, cc = e % NBD_EROW_COLS;
+            const int64_t i = ilo + rr, j = jc + cc;
+            if (r0 + rr < nloc && j > i && j < N) {
+                const double dx = dsub(q[3 * j], q[3 * i]);
+                const double dy = dsub(q[3 * j + 1], q[3 * i + 1]);
+                const double dz = dsub(q[3 * j + 2], q[3 * i + 2]);
+                const double r2 = dfma(dz, dz, dfma(dy, dy, dfma(dx, dx, eps2)));
+                T[rr][cc] = -ddiv(dmul(G, dmul(mass[i], mass[j])), dsqrt(r2));
+            }
+        }
+        __syncthreads();
+        if (tx < NBD_EROW_ROWS && r0 + tx < nloc) {
+            const int64_t i = ilo + tx;
+            const int64_t c0 = (i + 1 > jc) ? i + 1 - jc : 0;
+            const int64_t c1 = (N - jc < NBD_EROW_COLS) ? N - jc : NBD_EROW_COLS;
+            for (int64_t cc = c0; cc < c1; ++cc) row.add(T[tx][cc]);
+        }
+        __syncthreads();
+    }
+    if (tx < NBD_EROW_ROWS && r0 + tx < nloc) slot[nloc + r0 + tx] = row.result();
 }
 
-__global__ void nbd_energy_sum_kernel(const double *terms, int P, int64_t nloc, double *out) {
+// One block: the terms are staged through shared memory in chunks by all threads
+// (coalesced), and thread 0 runs the compensated sum over each chunk in order --
+// the oracle's order (every kinetic term, then every row, shard by shard), so the
+// same bits as one thread reading global memory, without a global-load latency
+// per term.  Launch with NBD_ESUM_THREADS threads.
+constexpr int NBD_ESUM_THREADS = 256, NBD_ESUM_CHUNK = 4096;
+__global__ void __launch_bounds__(NBD_ESUM_THREADS) nbd_energy_sum_kernel(const double *terms, int P, int64_t nloc,
+                                                                          double *out) {
+    __shared__ double buf[NBD_ESUM_CHUNK];
+    const int64_t total = 2 * (int64_t)P * nloc;
     Neumaier tot;
-    for (int s = 0; s < P; ++s)
-        for (int64_t r = 0; r < nloc; ++r) tot.add(terms[(int64_t)s * 2 * nloc + r]);
-    for (int s = 0; s < P; ++s)
-        for (int64_t r = 0; r < nloc; ++r) tot.add(terms[(int64_t)s * 2 * nloc + nloc + r]);
-    *out = tot.result();
+    for (int64_t k0 = 0; k0 < total; k0 += NBD_ESUM_CHUNK) {
+        const int n = (int)((total - k0) < NBD_ESUM_CHUNK ? (total - k0) : NBD_ESUM_CHUNK);
+        for (int t = threadIdx.x; t < n; t += blockDim.x) {
+            const int64_t k = k0 + t, half = (int64_t)P * nloc;  // k-th term of the summation order
+            const int64_t kk = k < half ? k : k - half, sh = kk / nloc, r = kk - sh * nloc;
+            buf[t] = terms[sh * 2 * nloc + (k < half ? 0 : nloc) + r];
+        }
+        __syncthreads();
+        if (threadIdx.x == 0)
+            for (int t = 0; t < n; ++t) tot.add(buf[t]);
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) *out = tot.result();
 }
 
 }  // namespace irk
