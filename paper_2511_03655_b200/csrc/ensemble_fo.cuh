@@ -363,7 +363,7 @@ __global__ void __maxnreg__(FO8_MAXREG) ens_fo8_kernel(const __grid_constant__ E
             k = 0;
 #pragma unroll
             for (int l = 0; l < D; ++l) m[l] = p[l] = kInf;
-            if (s == 0) {
+            if ((sample || a.local_energy) && s == 0) {  // (sample test first: no divergent branch per step)
                 if (sample && ((a.c0 + n) % a.energy_every) == 0)
                     a.energy[((a.c0 + n) / a.energy_every) * B + b] = prob.energy(y, y + d);
                 if (a.local_energy) dhloc_update(prob.energy(y, y + d), hprev, dhmax);

@@ -287,7 +287,7 @@ __global__ void __maxnreg__(G8_MAXREG) ens_gs_kernel(const __grid_constant__ Ens
             k = 0;
 #pragma unroll
             for (int l = 0; l < d; ++l) m[l] = p[l] = kInfBits;
-            if (s == 0) {
+            if ((sample || a.local_energy) && s == 0) {  // (sample test first: no divergent branch per step)
                 if (sample && ((a.c0 + n) % a.energy_every) == 0)
                     a.energy[((a.c0 + n) / a.energy_every) * B + b] = prob.energy(q, v);
                 if (a.local_energy) dhloc_update(prob.energy(q, v), hprev, dhmax);

@@ -467,7 +467,7 @@ __global__ void __maxnreg__(N8M_MAXREG) ens_nbody8m_kernel(const __grid_constant
             for (int i = 0; i < NO; ++i) m[i] = p[i] = kInfBits;
         }
         const int64_t nloc = c * qa.qchunk + n;
-        if (fin && s == 0) {
+        if (fin && (sample || a.local_energy) && s == 0) {  // (sample test first: no divergent branch per step)
             const bool due = sample && (nloc % a.energy_every) == 0;
             if (due || a.local_energy) {
                 const double hn = n8m_energy<NB>(qv, qv + VO, P);
