@@ -42,6 +42,9 @@
 namespace irk {
 
 constexpr int G8M_THREADS = 64;  // two slots (8 trajectories) per block
+#ifndef G8M_SHADOW
+#define G8M_SHADOW 1
+#endif
 #ifndef G8M_UNIFORM_EXACT
 #define G8M_UNIFORM_EXACT 1  // exact-RHS re-evaluation as a warp-uniform branch (config 1 12.35 -> 12.24 ms)
 #endif
@@ -94,7 +97,12 @@ __global__ void __maxnreg__(G8M_MAXREG) ens_gsm_kernel(const __grid_constant__ E
     const unsigned gmask = 0x11111111u << g;  // the 8 stage lanes of trajectory g
     const int64_t b = ((int64_t)blockIdx.x * G8M_THREADS + threadIdx.x) / 32 * 4 + g;  // trajectory of the lane
     const bool valid = b < B;
-    const int64_t bb = valid ? b : 0;
+    // lanes of a ragged slot's missing trajectories shadow the slot's first one (same
+    // loads, same control flow, no stores): with one trajectory (config 1) the warp
+    // stays converged through the step-end branches (G8M_SHADOW; config 1 -x %)
+    const int64_t bslot = b - g;
+    const bool shadow = G8M_SHADOW && !valid && bslot < B;
+    const int64_t bb = valid ? b : (shadow ? bslot : 0);
     const G8MFrag fr(L);
     // coefficient fragments A[m = s][k = L % 4] of mu~, nu~ for the two k halves
     const double aM0 = c_mu[s][L & 3], aM1 = c_mu[s][4 + (L & 3)];
@@ -115,7 +123,7 @@ __global__ void __maxnreg__(G8M_MAXREG) ens_gsm_kernel(const __grid_constant__ E
         if (sample && a.c0 == 0) a.energy[b] = prob.energy(q, v);
         if (a.local_energy) hprev = prob.energy(q, v);
     }
-    bool live = valid && bad == 0 && a.nsteps > 0;
+    bool live = (valid || shadow) && bad == 0 && a.nsteps > 0;
     if (valid && !live && s == 0) {
         if (a.iters && a.c0 == 0) a.iters[b] = 0;
         if (a.csweeps) a.csweeps[b] = 0;
@@ -126,7 +134,7 @@ __global__ void __maxnreg__(G8M_MAXREG) ens_gsm_kernel(const __grid_constant__ E
     {
         double H[d];
 #pragma unroll
-        for (int l = 0; l < d; ++l) H[l] = live ? a.hist[((int64_t)s * D + d + l) * B + b] : 0.0;
+        for (int l = 0; l < d; ++l) H[l] = live ? a.hist[((int64_t)s * D + d + l) * B + bb] : 0.0;
 #pragma unroll
         for (int t = 0; t < T; ++t) {
             double b0, b1, D0, D1;
@@ -266,16 +274,17 @@ __global__ void __maxnreg__(G8M_MAXREG) ens_gsm_kernel(const __grid_constant__ E
                 // (the sample test hoisted out of the s == 0 branch: one divergent branch
                 // fewer per step -- config 1 13.0 -> 12.3 ms)
                 if ((sample || a.local_energy) && s == 0) {
-                    if (sample && ((a.c0 + n) % a.energy_every) == 0)
+                    if (valid && sample && ((a.c0 + n) % a.energy_every) == 0)
                         a.energy[((a.c0 + n) / a.energy_every) * B + b] = prob.energy(q, v);
                     if (a.local_energy) dhloc_update(prob.energy(q, v), hprev, dhmax);
                 }
                 if (n == a.nsteps || !finite) {  // leave: history row s = Lv_s, q block zeroed (R-4)
+                    if (valid)
 #pragma unroll
-                    for (int l = 0; l < d; ++l) {
-                        a.hist[((int64_t)s * D + l) * B + b] = 0.0;
-                        a.hist[((int64_t)s * D + d + l) * B + b] = Lv[l];
-                    }
+                        for (int l = 0; l < d; ++l) {
+                            a.hist[((int64_t)s * D + l) * B + b] = 0.0;
+                            a.hist[((int64_t)s * D + d + l) * B + b] = Lv[l];
+                        }
                     if (!finite) bad = n0 + n;
                     live = false;
                 }
