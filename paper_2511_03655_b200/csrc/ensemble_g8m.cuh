@@ -42,6 +42,9 @@
 namespace irk {
 
 constexpr int G8M_THREADS = 64;  // two slots (8 trajectories) per block
+#ifndef G8M_SKIPK1
+#define G8M_SKIPK1 0  // 1: skip the stop-test work on sweeps where no trajectory tests (config 1 16.5 vs 11.9 ms)
+#endif
 #ifndef G8M_SHADOW
 #define G8M_SHADOW 1
 #endif
@@ -174,21 +177,27 @@ __global__ void __maxnreg__(G8M_MAXREG) ens_gsm_kernel(const __grid_constant__ E
         // sweep's (m, p) ----
         int64_t delta[d];
         bool okb = true;  // (BALLOT) this sweep's R2 decision from ballots
+        // (BALLOT: nothing here is used on a step's first sweep, k = 1 -- skipped when
+        // no trajectory of the slot tests; warp-uniform with one trajectory)
+        const bool anyk2 = !(BALLOT && G8M_SKIPK1) || __any_sync(FULL, live && k >= 2);
 #pragma unroll
         for (int l = 0; l < d; ++l) {
-            int64_t e = dabs_bits(dsub(Q[l], Qold[l]));
-            e = (e > kInfBits) ? 0 : e;  // NaN-ignoring max (canonical left-to-right form)
-            Qold[l] = Q[l];
-            if constexpr (BALLOT) {
-            const unsigned nz = __ballot_sync(FULL, e != 0) & gmask;
-            const unsigned ge = __ballot_sync(FULL, e >= m[l]) & gmask;
-            okb = okb & ((nz == 0u) | ((m[l] <= p[l]) & (ge != 0u)));
-            }
+            int64_t e = 0;
+            if (anyk2) {
+                e = dabs_bits(dsub(Q[l], Qold[l]));
+                e = (e > kInfBits) ? 0 : e;  // NaN-ignoring max (canonical left-to-right form)
+                if constexpr (BALLOT) {
+                    const unsigned nz = __ballot_sync(FULL, e != 0) & gmask;
+                    const unsigned ge = __ballot_sync(FULL, e >= m[l]) & gmask;
+                    okb = okb & ((nz == 0u) | ((m[l] <= p[l]) & (ge != 0u)));
+                }
 #pragma unroll
-            for (int off = 4; off < 32; off <<= 1) {
-                const int64_t o = __shfl_xor_sync(FULL, e, off);
-                e = (o > e) ? o : e;
+                for (int off = 4; off < 32; off <<= 1) {
+                    const int64_t o = __shfl_xor_sync(FULL, e, off);
+                    e = (o > e) ? o : e;
+                }
             }
+            Qold[l] = Q[l];
             delta[l] = e;
         }
         // ---- a3: F_s = g(Q_s, t_{n-1} + c_s h) ----
