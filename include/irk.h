@@ -74,13 +74,16 @@ enum irk_option {
     IRK_OPT_MAPPING = 4,      /* Kepler / Henon-Heiles (partitioned mode): IRK_MAP_AUTO (default),
                                  IRK_MAP_G1 = one trajectory per thread, IRK_MAP_G2 / IRK_MAP_G4 =
                                  2 / 4 lanes per trajectory (4 / 2 stages per lane), IRK_MAP_G8 = 8 lanes per
-                                 trajectory, one stage per lane (warp-shuffle contractions and
-                                 convergence reduction).  IRK_NBODY: IRK_MAP_G1 = body per lane,
+                                 trajectory, one stage per lane (shared-memory all-gather, shuffle
+                                 convergence reduction), IRK_MAP_G8M = one stage per lane with both
+                                 stage contractions on the FP64 tensor core (DMMA m8n8k4 on shuffled
+                                 fragments; ensemble_g8m.cuh; auto for small batches).  In
+                                 first-order mode G8M falls back to G1.  IRK_NBODY: IRK_MAP_G1 = body per lane,
                                  IRK_MAP_G8 = stage per lane (shared-memory all-gather),
                                  IRK_MAP_G8M = stage per lane with the two stage contractions on
                                  the FP64 tensor core (DMMA m8n8k4; ensemble_nbody8m.cuh).  Auto
                                  picks by problem, N and batch size from measured crossovers
-                                 ("ens_gs", "ens_nbody8", "ens_nbody8m"; the chunked IRK_OPT_SCHEDULE = 1 keeps
+                                 ("ens_gs", "ens_gsm", "ens_nbody8", "ens_nbody8m"; the chunked IRK_OPT_SCHEDULE = 1 keeps
                                  body per lane).  Bitwise-neutral.  */
     IRK_OPT_BALANCE = 5,      /* ensemble scheduling: -1 = auto (default), 0 = off, C > 0 = run the
                                  call in chunks of C steps, re-sorting trajectories by the cost of

@@ -3,6 +3,7 @@
 set -x
 mkdir -p gpurun_out
 timeout 1500 python -m pytest tests -m gpu -q > gpurun_out/pytest_final.log 2>&1; echo pytest rc=$?
+timeout 300 python -c 'import __graft_entry__ as g; g.smoke()' > gpurun_out/smoke_final.log 2>&1; echo smoke rc=$?; cat gpurun_out/smoke_final.log | tail -2
 tail -3 gpurun_out/pytest_final.log
 timeout 600 python bench.py > gpurun_out/bench_final.json 2> gpurun_out/bench_final.err; echo bench rc=$?
 cat gpurun_out/bench_final.json
