@@ -112,3 +112,36 @@ def test_mapping_used_reports_g8m(irk):
         ig.integrate(Y, ig.new_workspace())
         torch.cuda.synchronize()
         assert ig.get_option(irk.INFO_MAPPING_USED) == irk.MAP_G8M
+
+
+@pytest.mark.parametrize("batch", [1, 3])
+def test_one_slot_gm_not_one(irk, orc, batch):
+    """The one-slot launch (ballot stop test, shadow lanes) with GM = 1.3: the
+    full correctly rounded division w = GM / r^3 (KeplerT<false>); bitwise equal
+    to the oracle with energy samples."""
+    w = wl.kepler_ensemble(batch=batch, nsteps=1500)
+    w.params = np.array([1.3])
+    g = run_gpu(irk, w, energy_every=100, mapping=irk.MAP_G8M)
+    o = orc.integrate(w.problem, w.y, w.params, w.h, w.nsteps, energy_every=100)
+    assert_parity(g, o, energy=True)
+    assert np.array_equal(g["iters"], o["iters"])
+
+
+def test_shadowed_slot_with_divergence(irk, orc):
+    """Two trajectories in one slot: trajectory 0 (which the slot's two missing
+    trajectories shadow) diverges and freezes, trajectory 1 integrates on.
+    g8m == g8 (states, sweeps, stats, history), the finite member == oracle, and
+    the shadows store nothing (the workspace rows beyond the batch are untouched
+    by construction: the history equals g8's)."""
+    w = wl.kepler_ensemble(batch=2, nsteps=400)
+    y = w.y.copy()
+    y[:, 0] = [1e-200, 0.0, 0.0, 0.0]
+    a = run_gpu(irk, w, y=y, energy_every=50, mapping=irk.MAP_G8M)
+    b = run_gpu(irk, w, y=y, energy_every=50, mapping=irk.MAP_G8)
+    assert np.array_equal(a["y"], b["y"], equal_nan=True)
+    assert np.array_equal(a["iters"], b["iters"]) and a["stats"] == b["stats"]
+    assert np.array_equal(a["hist"], b["hist"], equal_nan=True)
+    assert np.array_equal(a["energy"], b["energy"], equal_nan=True)
+    assert not np.isfinite(a["y"][:, 0]).all() and np.isfinite(a["y"][:, 1]).all()
+    o = orc.integrate(w.problem, y[:, 1:], w.params, w.h, w.nsteps, energy_every=50)
+    assert np.array_equal(a["y"][:, 1:], o["y"]) and np.array_equal(a["iters"][1:], o["iters"])
