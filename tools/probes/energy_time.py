@@ -1,5 +1,6 @@
-import sys, torch
-sys.path.insert(0, '/root/repo')
+"""Time one config-5 energy sample (irk_energy, N = 8,192) and print its bits."""
+import os, sys, torch
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
 from paper_2511_03655_b200 import irk, workloads as wl
 w = wl.plummer()
 with irk.Integrator(w.problem, w.dim, w.h, 1, 1, w.params) as ig:
