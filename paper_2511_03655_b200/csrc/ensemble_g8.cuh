@@ -33,6 +33,9 @@ constexpr int G8_THREADS = 64;  // 8 trajectories per block
 #ifndef G8_SMEM
 #define G8_SMEM 1  // all-gathers through a shared-memory tile (0: shuffles; 2,000 steps at B = 512: 3.65 vs 4.65 ms)
 #endif
+#ifndef GS_UNIFORM_EXACT
+#define GS_UNIFORM_EXACT 1  // exact-RHS re-evaluation as a warp-uniform branch (g4 at 8,192: 23.2 -> 22.5 ms)
+#endif
 #ifndef G8_MAXREG
 #define G8_MAXREG 168  // g8 uses 119 (B = 2048: 80 regs 5.8 ms, 96: 5.2, 119: 3.7); g4 / g2 use 124 / 156 (at 128 g2 spilled: 7.35 vs 6.88 ms at 8,192)
 #endif
@@ -203,7 +206,11 @@ __global__ void __maxnreg__(G8_MAXREG) ens_gs_kernel(const __grid_constant__ Ens
 #pragma unroll
             for (int t = 0; t < SPL; ++t)
                 prob.template accel<false>(Qs[t], Fs[t], dadd(tn1, dmul(sC[st0 + t], a.h)), ok);
+#if GS_UNIFORM_EXACT
+            if (__any_sync(FULL, !ok && live))  // exact slow path, same bits (warp-uniform)
+#else
             if (!ok && live)  // exact slow path, same bits (live groups only)
+#endif
 #pragma unroll
                 for (int t = 0; t < SPL; ++t)
                     prob.template accel<true>(Qs[t], Fs[t], dadd(tn1, dmul(sC[st0 + t], a.h)), ok);

@@ -67,6 +67,9 @@ constexpr int N8M_THREADS = 32 * N8M_WARPS;  // one slot of 4 trajectories per w
 #ifndef N8M_CMASS
 #define N8M_CMASS 1  // masses read from the kernel parameters instead of shared memory (with DREUSE 2: config 3, 2,000 steps 60.2 -> 58.4 ms)
 #endif
+#ifndef N8M_UNIFORM_EXACT
+#define N8M_UNIFORM_EXACT 0
+#endif
 #ifndef N8M_A2SYNC
 #define N8M_A2SYNC 0
 #endif
@@ -422,7 +425,11 @@ __global__ void __maxnreg__(N8M_MAXREG) ens_nbody8m_kernel(const __grid_constant
 #else
             n8_accel<NB, false, G1>(Qs, F, P, sm, ok);
 #endif
+#if N8M_UNIFORM_EXACT
+            if (__any_sync(FULL, !ok && live)) {  // exact intrinsics, same bits (out of line, rare; warp-uniform)
+#else
             if (!ok && live) {  // exact intrinsics, same bits (out of line, rare)
+#endif
                 double row[d];
 #pragma unroll
                 for (int l = 0; l < d; ++l) row[l] = Qs[l];
