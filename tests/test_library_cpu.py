@@ -84,10 +84,13 @@ def test_params_and_options_errors(irk):
     with pytest.raises(irk.IrkError):  # first-order mode is built for the per-thread problems only
         irk.Integrator(irk.FPU_BETA, 128, 0.1, 10, 4, params=[1.0], mode=irk.FIRST_ORDER)
     irk.Integrator(irk.HENON_HEILES, 4, 0.1, 10, 4, params=[1.0, 0.0], mode=irk.FIRST_ORDER).close()
-    for mp in (irk.MAP_AUTO, irk.MAP_G1, irk.MAP_G2, irk.MAP_G4, irk.MAP_G8):  # lanes per trajectory
+    for mp in (irk.MAP_AUTO, irk.MAP_G1, irk.MAP_G2, irk.MAP_G4, irk.MAP_G8, irk.MAP_G8M):  # lanes per trajectory
         k = irk.Integrator(irk.KEPLER, 4, 0.1, 10, 4, params=[1.0], mapping=mp)
         assert k.get_option(irk.OPT_MAPPING) == mp
         k.close()
+    irk.Integrator(irk.HENON_HEILES, 4, 0.1, 10, 4, params=[1.0, 0.1], mapping=irk.MAP_G8M).close()
+    with pytest.raises(irk.IrkError):  # g8m: Kepler, Henon-Heiles and the N-body ensembles only
+        irk.Integrator(irk.FPU_BETA, 128, 0.1, 10, 4, params=[1.0], mapping=irk.MAP_G8M)
     for mp in (3, 16):
         with pytest.raises(irk.IrkError):
             irk.Integrator(irk.KEPLER, 4, 0.1, 10, 4, params=[1.0], mapping=mp)
