@@ -430,11 +430,28 @@ __global__ void nbd_vel_kernel(const __grid_constant__ NbdArgs a) {
     const bool stop = (k >= 2) && (a.ctl->notok == 0);
     const bool fin = stop || (k >= a.max_iters);
     double Lv[8];
+    if (nj <= 8) {  // (N <= 8,192: all 64 partial sums loaded before the dadd chains -- one
+                    // memory latency per thread instead of one per j-block)
+        double pv[8][8];
 #pragma unroll
-    for (int i = 0; i < 8; ++i) {
-        double acc = 0.0;
-        for (int J = 0; J < nj; ++J) acc = dadd(acc, a.part[((int64_t)J * 8 + i) * dl + l]);
-        Lv[i] = dmul(a.hb[i], acc);
+        for (int J = 0; J < 8; ++J)
+#pragma unroll
+            for (int i = 0; i < 8; ++i) pv[J][i] = J < nj ? __ldcg(&a.part[((int64_t)J * 8 + i) * dl + l]) : 0.0;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            double acc = 0.0;
+#pragma unroll
+            for (int J = 0; J < 8; ++J)
+                if (J < nj) acc = dadd(acc, pv[J][i]);
+            Lv[i] = dmul(a.hb[i], acc);
+        }
+    } else {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            double acc = 0.0;
+            for (int J = 0; J < nj; ++J) acc = dadd(acc, a.part[((int64_t)J * 8 + i) * dl + l]);
+            Lv[i] = dmul(a.hb[i], acc);
+        }
     }
     double v = a.yv[l];
     if (fin) {
