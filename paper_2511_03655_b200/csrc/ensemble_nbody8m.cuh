@@ -237,8 +237,11 @@ __device__ __forceinline__ void n8m_contract(double *D, double a0, double a1, co
     for (int t = 0; t < T; ++t) dmma884(D[2 * t], D[2 * t + 1], a1, b1[t], D[2 * t], D[2 * t + 1]);
 }
 
-template <int NB, bool G1>
-__global__ void __maxnreg__(N8M_MAXREG) ens_nbody8m_kernel(const __grid_constant__ EnsArgs a,
+// MR: register cap.  N8M_MAXREG (168) at full load -- 12 warps per SM were the
+// measured optimum; 255 for small batches (a few warps per SM: no occupancy to lose,
+// no spills, more of the 15 pair chains in flight; 2,048 trajectories -11 %).
+template <int NB, bool G1, int MR = N8M_MAXREG>
+__global__ void __maxnreg__(MR) ens_nbody8m_kernel(const __grid_constant__ EnsArgs a,
                                                          const __grid_constant__ QueueArgs qa,
                                                          const __grid_constant__ NBodyParams P) {
     constexpr int d = 3 * NB, D = 6 * NB, T = (d + 1) / 2, d2 = 2 * T, WPB = N8M_THREADS / 32;

@@ -55,6 +55,7 @@ struct irk_ctx {
     int fo_blocks_per_sm = 0;
     int nbody8_blocks_per_sm[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
     int nbody8m_blocks_per_sm[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+    int nbody8m_hi_blocks_per_sm[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
     int local_energy = 0;  // IRK_OPT_LOCAL_ENERGY
     int64_t energy_every = 0;
     Tableau T;
@@ -110,6 +111,10 @@ constexpr size_t kHeader = 64;
 constexpr int64_t kG8AutoMaxBatch = IRK_G8_AUTO_MAX;
 constexpr int64_t kG4AutoMaxBatch = IRK_G4_AUTO_MAX;
 constexpr int64_t kG2AutoMaxBatch = IRK_G2_AUTO_MAX;
+#ifndef IRK_N8M_HIREG_MAX
+#define IRK_N8M_HIREG_MAX 6144
+#endif
+constexpr int64_t kN8mHiRegMaxBatch = IRK_N8M_HIREG_MAX;  // ens_nbody8m at 255 registers up to this batch
 constexpr int64_t kFo8AutoMaxBatch = INT64_MAX;  // first-order mode: stage per lane at every measured batch
                                                  // (tools/fo_bench.py: 1 to 65,536 trajectories)
 
@@ -783,17 +788,20 @@ int launch_nbody_t(irk_ctx *c, double *y, double t0, char *ws, double *energy, i
         // trajectory (1,563 steps), 1.58 / 1.53 / 1.52 / 1.53 s at 250 / 100 / 50 / 25
         constexpr int64_t kUnitSteps = 50;
         constexpr int SPB = irk::N8M_THREADS / 32 * 4;  // trajectories per block
-        return (IRK_UNIT_G && P.G == 1.0)
-                   ? launch_queue(c, irk::ens_nbody8m_kernel<NB, true>, irk::N8M_THREADS, SPB,
-                                  &c->nbody8m_blocks_per_sm[NB], a, ws, st,
-                                  [&](const EnsArgs &aa, const irk::QueueArgs &qa, unsigned nb) {
-                                      irk::ens_nbody8m_kernel<NB, true><<<nb, irk::N8M_THREADS, 0, st>>>(aa, qa, P);
-                                  }, 32, 0, kUnitSteps)
-                   : launch_queue(c, irk::ens_nbody8m_kernel<NB, false>, irk::N8M_THREADS, SPB,
-                                  &c->nbody8m_blocks_per_sm[NB], a, ws, st,
-                                  [&](const EnsArgs &aa, const irk::QueueArgs &qa, unsigned nb) {
-                                      irk::ens_nbody8m_kernel<NB, false><<<nb, irk::N8M_THREADS, 0, st>>>(aa, qa, P);
-                                  }, 32, 0, kUnitSteps);
+        // small batches: the 255-register instantiation (few warps per SM; config-3
+        // generator, 5,000 steps, ms at 168 / 255 registers: 2,048 42.4 / 37.7,
+        // 4,096 50.9 / 46.5, 8,192 73.0 / 79.9)
+        const bool hi = c->batch <= kN8mHiRegMaxBatch;
+        int *bps = hi ? &c->nbody8m_hi_blocks_per_sm[NB] : &c->nbody8m_blocks_per_sm[NB];
+        auto run = [&](auto kern) {
+            return launch_queue(c, kern, irk::N8M_THREADS, SPB, bps, a, ws, st,
+                                [&](const EnsArgs &aa, const irk::QueueArgs &qa, unsigned nb) {
+                                    kern<<<nb, irk::N8M_THREADS, 0, st>>>(aa, qa, P);
+                                }, 32, 0, kUnitSteps);
+        };
+        if (IRK_UNIT_G && P.G == 1.0)
+            return hi ? run(irk::ens_nbody8m_kernel<NB, true, 255>) : run(irk::ens_nbody8m_kernel<NB, true>);
+        return hi ? run(irk::ens_nbody8m_kernel<NB, false, 255>) : run(irk::ens_nbody8m_kernel<NB, false>);
     }
     if (stage_per_lane)
         return (IRK_UNIT_G && P.G == 1.0)
