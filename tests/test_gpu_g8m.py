@@ -145,3 +145,26 @@ def test_shadowed_slot_with_divergence(irk, orc):
     assert not np.isfinite(a["y"][:, 0]).all() and np.isfinite(a["y"][:, 1]).all()
     o = orc.integrate(w.problem, y[:, 1:], w.params, w.h, w.nsteps, energy_every=50)
     assert np.array_equal(a["y"][:, 1:], o["y"]) and np.array_equal(a["iters"][1:], o["iters"])
+
+
+@pytest.mark.parametrize("batch", [1, 4])
+def test_one_slot_local_energy_chained(irk, orc, batch):
+    """One slot (ballot stop test, shadow lanes) with Delta H^loc (Eq. DHlocmax)
+    and energy samples over two chained calls: bitwise equal to the oracle."""
+    w = wl.kepler_ensemble(batch=batch, nsteps=800)
+    with irk.Integrator(w.problem, w.dim, w.h, w.nsteps // 2, w.batch, w.params, energy_every=40,
+                        mapping=irk.MAP_G8M, local_energy=True) as ig:
+        Y = torch.tensor(w.y, dtype=torch.float64, device="cuda")
+        ws = ig.new_workspace()
+        E = torch.zeros((ig.n_energy(), w.batch), dtype=torch.float64, device="cuda")
+        it = torch.zeros(w.batch, dtype=torch.int64, device="cuda")
+        ig.integrate(Y, ws, energy=E, iters=it)
+        E1, it1, d1 = E.cpu().numpy().copy(), it.cpu().numpy().copy(), ig.local_energy_error(ws).cpu().numpy()
+        ig.integrate(Y, ws, energy=E, iters=it)
+        y2, E2, it2, d2 = Y.cpu().numpy(), E.cpu().numpy(), it.cpu().numpy(), ig.local_energy_error(ws).cpu().numpy()
+    o1 = orc.integrate(w.problem, w.y, w.params, w.h, w.nsteps // 2, energy_every=40, local_energy=True)
+    o2 = orc.integrate(w.problem, o1["y"], w.params, w.h, w.nsteps // 2, energy_every=40, local_energy=True,
+                       n0=w.nsteps // 2, hist=o1["hist"])
+    assert np.array_equal(E1, o1["energy"]) and np.array_equal(d1, o1["dhloc"]) and np.array_equal(it1, o1["iters"])
+    assert np.array_equal(y2, o2["y"]) and np.array_equal(E2, o2["energy"])
+    assert np.array_equal(d2, o2["dhloc"]) and np.array_equal(it2, o2["iters"])
